@@ -1,0 +1,221 @@
+"""Quantized sparse self-attention (reference: attention.py) on the B200 pipeline.
+
+softmax(Q K^T (masked) / sqrt(d)) V with symmetric absmax quantization, an
+SDDMM with fused dequant, a float softmax with fused requant, and an SpMM with
+fused dequant -- all in libmcube (mc_sparse_attention). `mode="parity"`
+reproduces the reference's float64 rounding chain; `mode="fast"` runs the
+softmax in float32 (stated tolerance: max-abs 1e-3 on the fp16 output).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, Tuple
+
+import numpy as np
+
+from . import _device as D
+from . import _native as N
+from .errors import UnsupportedPrecisionError
+from .qint import ROW_MAJOR, PackedArray, PackedMatrix, pack_dense
+from .sparse_format import BcrsMatrix
+
+SUPPORTED_PRECISIONS = ((16, 8), (8, 8), (8, 4))
+MASK_VECTOR_LENGTH = 8
+FAST_MODE_TOLERANCE = 1e-3  # max-abs on the fp16 output, fast (fp32 softmax) mode
+
+
+@dataclass(frozen=True)
+class QuantizationParams:
+    scale: float
+    bit_width: int
+    signed: bool = True
+
+
+def quantize(x, bits: int, calibration: str = "absmax", layout: str = ROW_MAJOR
+             ) -> Tuple[PackedMatrix, QuantizationParams]:
+    """Symmetric absmax quantization (attention.py:40-56): scale = absmax/(2^(b-1)-1),
+    ties to even, all-zero input -> scale 1. Host helper (the fused pipeline
+    quantizes on the device with the same float64 arithmetic)."""
+    if calibration != "absmax":
+        raise ValueError(f"unknown calibration {calibration!r}")
+    arr = np.asarray(x.detach().cpu() if D.is_torch(x) else x, dtype=np.float64)
+    if not np.isfinite(arr).all():
+        raise ValueError("input must be finite")
+    qmax = (1 << (bits - 1)) - 1
+    absmax = float(np.abs(arr).max()) if arr.size else 0.0
+    scale = absmax / qmax if absmax > 0 else 1.0
+    q = np.clip(np.rint(arr / scale), -qmax, qmax).astype(np.int64)
+    return pack_dense(q, bits, layout), QuantizationParams(scale, bits)
+
+
+def dequantize(q, params: QuantizationParams) -> np.ndarray:
+    return np.asarray(q, dtype=np.float64) * params.scale
+
+
+@dataclass(frozen=True, eq=False)
+class AttentionConfig:
+    seq_len: int
+    softmax_bits: int
+    qkv_bits: int
+    mask: BcrsMatrix
+    head_dim: int = 64
+    num_heads: int = 1
+
+    def __post_init__(self):
+        if self.seq_len % MASK_VECTOR_LENGTH:
+            raise ValueError(f"sequence length must be a multiple of {MASK_VECTOR_LENGTH}")
+        if (self.softmax_bits, self.qkv_bits) not in SUPPORTED_PRECISIONS:
+            names = [f"{a}b-{b}b" for a, b in SUPPORTED_PRECISIONS]
+            raise UnsupportedPrecisionError(
+                f"{self.softmax_bits}b-{self.qkv_bits}b not in supported set {names}")
+        if self.mask.vector_length != MASK_VECTOR_LENGTH:
+            raise ValueError("attention mask must use 8x1 blocks")
+        if self.mask.scalar_rows != self.seq_len or self.mask.scalar_cols != self.seq_len:
+            raise ValueError("mask must be seq_len x seq_len")
+
+    @property
+    def softmax_scale(self) -> float:
+        return 1.0 / ((1 << (self.softmax_bits - 1)) - 1)
+
+
+@dataclass(frozen=True, eq=False)
+class AttentionResult:
+    output: object
+    scores_int: object
+    scores: BcrsMatrix
+    probs: BcrsMatrix
+    probs_int: BcrsMatrix
+    mix_int: object
+    params: Dict[str, QuantizationParams]
+
+
+_DTYPES = {"float16": N.MC_DTYPE_F16, "float32": N.MC_DTYPE_F32, "float64": N.MC_DTYPE_F64}
+
+
+def _input(x):
+    t = D.torch()
+    if D.is_torch(x):
+        tt = x.cuda().contiguous()
+    else:
+        arr = np.ascontiguousarray(np.asarray(x))
+        if arr.dtype not in (np.float16, np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        tt = t.from_numpy(arr).cuda()
+    name = str(tt.dtype).replace("torch.", "")
+    if name not in _DTYPES:
+        tt = tt.to(t.float64)
+        name = "float64"
+    return tt, _DTYPES[name]
+
+
+class AttentionRunner:
+    """Reusable launcher for batched attention over one shared mask.
+
+    Holds the device mask and a workspace sized for (batch, cfg); call() is
+    stream-ordered and does no host synchronisation unless check=True.
+    """
+
+    def __init__(self, cfg: AttentionConfig, batch: int, mode: str = "fast", stages: bool = False):
+        t = D.torch()
+        self.cfg, self.batch, self.stages = cfg, batch, stages
+        self.mode = N.MC_ATTN_FAST if mode == "fast" else N.MC_ATTN_PARITY
+        self.mask, self._keep = D.bcrs_struct(cfg.mask)
+        self.nblk8 = cfg.mask.n_blocks * 8
+        self.args = N.McAttentionArgs()
+        a = self.args
+        a.batch, a.seq_len, a.head_dim = batch, cfg.seq_len, cfg.head_dim
+        a.softmax_bits, a.qkv_bits, a.mode = cfg.softmax_bits, cfg.qkv_bits, self.mode
+        a.mask = N.ctypes.pointer(self.mask)
+        a.in_dtype = N.MC_DTYPE_F16
+        size = N.ctypes.c_size_t(0)
+        N.check(N.lib().mc_attention_workspace(N.ctypes.byref(a), N.ctypes.byref(size)))
+        self.workspace = t.empty(max(int(size.value), 1), dtype=t.uint8, device="cuda")
+        a.workspace, a.workspace_bytes = N.ptr(self.workspace), int(size.value)
+        L, d = cfg.seq_len, cfg.head_dim
+        self.out = t.empty((batch, L, d), dtype=t.float16, device="cuda")
+        self.scales = t.empty((batch, 4), dtype=t.float64, device="cuda")
+        a.out_f16, a.scales = N.ptr(self.out), N.ptr(self.scales)
+        if stages:
+            self.scores_int = t.empty((batch, self.nblk8), dtype=t.int32, device="cuda")
+            self.scores_f16 = t.empty((batch, self.nblk8), dtype=t.float16, device="cuda")
+            self.probs_f16 = t.empty((batch, self.nblk8), dtype=t.float16, device="cuda")
+            self.probs_int = t.empty((batch, self.nblk8), dtype=t.int32, device="cuda")
+            self.mix_int = t.empty((batch, L, d), dtype=t.int32, device="cuda")
+            a.scores_int, a.scores_f16 = N.ptr(self.scores_int), N.ptr(self.scores_f16)
+            a.probs_f16, a.probs_int = N.ptr(self.probs_f16), N.ptr(self.probs_int)
+            a.mix_int = N.ptr(self.mix_int)
+
+    def __call__(self, q, k, v, stream=None, check: bool = False):
+        qd, dt = _input(q)
+        kd = _input(k)[0].to(qd.dtype)
+        vd = _input(v)[0].to(qd.dtype)
+        expect = (self.batch, self.cfg.seq_len, self.cfg.head_dim)
+        for x in (qd, kd, vd):
+            if tuple(x.shape[-2:]) != expect[1:] or x.numel() != int(np.prod(expect)):
+                raise ValueError(f"Q, K, V must be {expect[1:]} per head, batch {self.batch}")
+        a = self.args
+        a.q, a.k, a.v, a.in_dtype = N.ptr(qd), N.ptr(kd), N.ptr(vd), dt
+        status = D.status_word()
+        N.check(N.lib().mc_sparse_attention(N.ctypes.byref(a), N.ptr(status), N.stream_ptr(stream)))
+        if check:
+            D.fetch_status(status, stream)
+        return self.out
+
+
+def batched_sparse_attention(q, k, v, cfg: AttentionConfig, mode: str = "fast"):
+    """[B, H, L, d] (or [H, L, d]) heads sharing cfg.mask -> fp16 output, same shape."""
+    qd, _ = _input(q)
+    lead = tuple(qd.shape[:-2])
+    batch = int(np.prod(lead)) if lead else 1
+    run = AttentionRunner(cfg, batch, mode=mode)
+    out = run(qd.reshape(batch, cfg.seq_len, cfg.head_dim), k if not D.is_torch(k) else
+              k.reshape(batch, cfg.seq_len, cfg.head_dim),
+              v if not D.is_torch(v) else v.reshape(batch, cfg.seq_len, cfg.head_dim), check=True)
+    return out.reshape(*lead, cfg.seq_len, cfg.head_dim)
+
+
+def _fp16_round(x) -> np.ndarray:
+    return np.asarray(x, dtype=np.float64).astype(np.float16).astype(np.float64)
+
+
+def sparse_attention(q, k, v, cfg: AttentionConfig, mode: str = "parity") -> AttentionResult:
+    """One head (attention.py:130-187), integer stages exposed like the reference."""
+    ld = (cfg.seq_len, cfg.head_dim)
+    shapes = [tuple(x.shape) if D.is_torch(x) else np.asarray(x).shape for x in (q, k, v)]
+    if any(s != ld for s in shapes):
+        raise ValueError(f"Q, K, V must be {ld}")
+    host = not D.is_torch(q)
+    run = AttentionRunner(cfg, 1, mode=mode, stages=True)
+    qd, _ = _input(q)
+    run(qd.reshape(1, *ld), _input(k)[0].reshape(1, *ld), _input(v)[0].reshape(1, *ld), check=True)
+    mask = cfg.mask
+    out = run.out[0].to(D.torch().float64)
+    scores_int, mix_int = run.scores_int[0], run.mix_int[0]
+    scores_f, probs_f = run.scores_f16[0].to(D.torch().float64), run.probs_f16[0].to(D.torch().float64)
+    probs_int = run.probs_int[0]
+    sc = run.scales[0].cpu().numpy()
+    if host:
+        out, scores_int, mix_int = out.cpu().numpy(), scores_int.cpu().numpy(), mix_int.cpu().numpy()
+        scores_f, probs_f, probs_int = scores_f.cpu().numpy(), probs_f.cpu().numpy(), probs_int.cpu().numpy()
+        probs_packed = PackedArray.from_values(probs_int, cfg.softmax_bits, signed=True)
+    else:
+        probs_packed = probs_int
+    mk = lambda vals: BcrsMatrix(mask.scalar_rows, mask.scalar_cols, 8, mask.row_offsets,
+                                 mask.col_indices, vals)
+    params = {"q": QuantizationParams(float(sc[0]), cfg.qkv_bits),
+              "k": QuantizationParams(float(sc[1]), cfg.qkv_bits),
+              "v": QuantizationParams(float(sc[2]), cfg.qkv_bits),
+              "softmax": QuantizationParams(cfg.softmax_scale, cfg.softmax_bits)}
+    return AttentionResult(output=out, scores_int=scores_int, scores=mk(scores_f), probs=mk(probs_f),
+                           probs_int=mk(probs_packed), mix_int=mix_int, params=params)
+
+
+def multi_head_attention(q, k, v, cfg: AttentionConfig, mode: str = "parity"):
+    """(heads, L, d) inputs, one shared mask (attention.py:190-197) -> (heads, L, d)."""
+    expect = (cfg.num_heads, cfg.seq_len, cfg.head_dim)
+    shp = tuple(q.shape) if D.is_torch(q) else np.asarray(q).shape
+    if shp != expect:
+        raise ValueError(f"expected stacked heads of shape {expect}")
+    out = batched_sparse_attention(q, k, v, cfg, mode=mode).to(D.torch().float64)
+    return out.cpu().numpy() if not D.is_torch(q) else out

@@ -1,0 +1,269 @@
+// attention.cu -- quantised sparse self-attention (attention.py:130-197) on B200.
+//
+// Pipeline per head (all heads share one 8x1 block mask, attention.py:190-197):
+//   quantize Q, K, V (symmetric absmax, attention.py:40-56)         -> quant kernels
+//   SDDMM Q_q K_q^T at the mask, fused dequant to fp16 (:147-154)   -> sddmm.cu
+//   row softmax over stored blocks + fused requant (:108-127, :157-162) -> softmax kernel
+//   SpMM probs (SR-BCRS) x V_q, fused dequant to fp16 (:164-176)    -> spmm.cu
+// Parity mode evaluates every rounding step exactly as the reference does
+// (float64 math, round-to-nearest-even into fp16, rint requant); fast mode runs
+// the softmax in float32.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mcube {
+
+cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaStream_t stream, size_t* ws_needed);
+
+namespace {
+
+__device__ __forceinline__ double load_in(const void* p, int dtype, int64_t i) {
+  if (dtype == MC_DTYPE_F16) return static_cast<double>(__half2float(reinterpret_cast<const __half*>(p)[i]));
+  if (dtype == MC_DTYPE_F32) return static_cast<double>(reinterpret_cast<const float*>(p)[i]);
+  return reinterpret_cast<const double*>(p)[i];
+}
+
+// grid (batch, 3): absmax of one [L x d] tensor -> scale (attention.py:52-54)
+__global__ void __launch_bounds__(512)
+absmax_kernel(const void* q, const void* k, const void* v, int dtype, int64_t n, int bits, double* scales,
+              int smax) {
+  const int64_t b = blockIdx.x;
+  const int which = blockIdx.y;
+  const void* src = which == 0 ? q : (which == 1 ? k : v);
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(load_in(src, dtype, b * n + i)));
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) {
+      const double qmax = static_cast<double>((1 << (bits - 1)) - 1);
+      scales[b * 4 + which] = m > 0.0 ? m / qmax : 1.0;
+      if (which == 0) scales[b * 4 + 3] = 1.0 / static_cast<double>(smax);
+    }
+  }
+}
+
+// one thread per output word of the packed [L x d] tensor
+__global__ void quant_kernel(const void* q, const void* k, const void* v, int dtype, int64_t n, int bits,
+                             const double* scales, uint32_t* out, int64_t words_per, int64_t batch) {
+  const int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int which = blockIdx.y;
+  if (w >= words_per * batch) return;
+  const int64_t b = w / words_per;
+  const int64_t wi = w - b * words_per;
+  const void* src = which == 0 ? q : (which == 1 ? k : v);
+  const double scale = scales[b * 4 + which];
+  const double qmax = static_cast<double>((1 << (bits - 1)) - 1);
+  const int per = 32 / bits;
+  uint32_t word = 0;
+  for (int e = 0; e < per; ++e) {
+    const int64_t i = wi * per + e;
+    if (i >= n) break;
+    double x = rint(load_in(src, dtype, b * n + i) / scale);
+    x = fmin(fmax(x, -qmax), qmax);
+    const uint32_t qv = static_cast<uint32_t>(static_cast<int32_t>(x)) & ((1u << bits) - 1u);
+    word |= qv << (e * bits);
+  }
+  out[(static_cast<int64_t>(which) * batch + b) * words_per + wi] = word;
+}
+
+__global__ void alpha_kernel(const double* scales, int64_t batch, int head_dim, double* alpha_s, double* alpha_m) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const double sq = scales[b * 4], sk = scales[b * 4 + 1], sv = scales[b * 4 + 2], ss = scales[b * 4 + 3];
+  alpha_s[b] = sq * sk / sqrt(static_cast<double>(head_dim));  // attention.py:147
+  alpha_m[b] = ss * sv;                                          // attention.py:169
+}
+
+__device__ __forceinline__ double h2d(uint16_t h) {
+  __half x;
+  *reinterpret_cast<uint16_t*>(&x) = h;
+  return static_cast<double>(__half2float(x));
+}
+
+// one warp per (head, vector row); lane owns blocks j = lane, lane+32, ...
+template <bool FAST>
+__global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int64_t nblk8, const int64_t* offs,
+                                       int64_t vrows, const int64_t* sr_begin, int S, int smax, int sbits,
+                                       uint32_t* sr_vals, int64_t sr_stride_words, uint16_t* probs_f16,
+                                       int32_t* probs_int, int64_t batch) {
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= batch * vrows) return;
+  const int64_t b = gw / vrows, r = gw - b * vrows;
+  const int64_t lo = offs[r], hi = offs[r + 1], nb = hi - lo;
+  const int64_t sbeg = sr_begin[r];
+  const int64_t stored = ((nb + S - 1) / S) * S;
+  const uint16_t* sc = scores + b * nblk8 + lo * 8;
+  uint8_t* sv8 = reinterpret_cast<uint8_t*>(sr_vals + b * sr_stride_words);
+  uint16_t* sv16 = reinterpret_cast<uint16_t*>(sr_vals + b * sr_stride_words);
+  const double sm_scale = 1.0 / static_cast<double>(smax);
+
+  double mx[8], sum[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) { mx[v] = -INFINITY; sum[v] = 0.0; }
+  for (int64_t j = lane; j < nb; j += 32) {
+    const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
+    const uint16_t* hs = reinterpret_cast<const uint16_t*>(&u);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) mx[v] = fmax(mx[v], h2d(hs[v]));
+  }
+#pragma unroll
+  for (int v = 0; v < 8; ++v)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx[v] = fmax(mx[v], __shfl_xor_sync(0xffffffffu, mx[v], o));
+  for (int64_t j = lane; j < nb; j += 32) {
+    const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
+    const uint16_t* hs = reinterpret_cast<const uint16_t*>(&u);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      if constexpr (FAST) sum[v] += static_cast<double>(__expf(static_cast<float>(h2d(hs[v]) - mx[v])));
+      else sum[v] += exp(h2d(hs[v]) - mx[v]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < 8; ++v)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum[v] += __shfl_xor_sync(0xffffffffu, sum[v], o);
+
+  for (int64_t j = lane; j < stored; j += 32) {
+    const int64_t pos = sbeg + j;
+    const int64_t s = pos / S, jj = pos - s * S;
+    if (j < nb) {
+      const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
+      const uint16_t* hs = reinterpret_cast<const uint16_t*>(&u);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        double e;
+        if constexpr (FAST) e = static_cast<double>(__expf(static_cast<float>(h2d(hs[v]) - mx[v])));
+        else e = exp(h2d(hs[v]) - mx[v]);
+        const uint16_t pf = f16_bits_rn(e / sum[v]);
+        double qd = rint(h2d(pf) / sm_scale);  // attention.py:158
+        qd = fmin(fmax(qd, -static_cast<double>(smax)), static_cast<double>(smax));
+        const int32_t qi = static_cast<int32_t>(qd);
+        const int64_t el = s * 8 * S + static_cast<int64_t>(v) * S + jj;
+        if (sbits == 8) sv8[el] = static_cast<uint8_t>(qi);
+        else sv16[el] = static_cast<uint16_t>(qi);
+        if (probs_f16) probs_f16[b * nblk8 + (lo + j) * 8 + v] = pf;
+        if (probs_int) probs_int[b * nblk8 + (lo + j) * 8 + v] = qi;
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int64_t el = s * 8 * S + static_cast<int64_t>(v) * S + jj;
+        if (sbits == 8) sv8[el] = 0;
+        else sv16[el] = 0;
+      }
+    }
+  }
+}
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+}  // namespace
+
+cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaStream_t stream, size_t* ws_needed) {
+  const int64_t B = a->batch, L = a->seq_len, d = a->head_dim;
+  const int sb = a->softmax_bits, qb = a->qkv_bits;
+  const int S = (sb % 8 == 0 && qb % 8 == 0) ? 16 : 32;  // plan(sb, qb).tile.k (attention.py:164-165)
+  const int64_t vrows = L / 8;
+  const int64_t nblk = a->mask->n_blocks;
+  const int64_t n = L * d;
+  const int64_t qwords = (n * qb + 31) / 32;
+  const int64_t max_stored = nblk + vrows * (S - 1);
+  const int64_t sr_words = (max_stored * 8 * sb + 31) / 32;
+
+  size_t off = 0;
+  const size_t o_qkv = off; off = align256(off + 3 * B * qwords * 4);
+  const size_t o_scales = off; off = align256(off + B * 4 * 8);
+  const size_t o_alpha = off; off = align256(off + B * 2 * 8);
+  const size_t o_scores = off; off = align256(off + B * nblk * 8 * 2);
+  const size_t o_begin = off; off = align256(off + vrows * 8);
+  const size_t o_end = off; off = align256(off + vrows * 8);
+  const size_t o_total = off; off = align256(off + 8);
+  const size_t o_idx = off; off = align256(off + max_stored * 4);
+  const size_t o_idx2 = off; off = align256(off + max_stored * 4);
+  const size_t o_sr = off; off = align256(off + B * sr_words * 4);
+  if (ws_needed) *ws_needed = off;
+  if (!a->workspace) return cudaSuccess;
+
+  uint8_t* ws = static_cast<uint8_t*>(a->workspace);
+  uint32_t* qkv = reinterpret_cast<uint32_t*>(ws + o_qkv);
+  double* scales = a->scales ? a->scales : reinterpret_cast<double*>(ws + o_scales);
+  double* alpha_s = reinterpret_cast<double*>(ws + o_alpha);
+  double* alpha_m = alpha_s + B;
+  uint16_t* scores = a->scores_f16 ? a->scores_f16 : reinterpret_cast<uint16_t*>(ws + o_scores);
+  int64_t* sr_begin = reinterpret_cast<int64_t*>(ws + o_begin);
+  int64_t* sr_end = reinterpret_cast<int64_t*>(ws + o_end);
+  int64_t* sr_total = reinterpret_cast<int64_t*>(ws + o_total);
+  uint32_t* sr_idx = reinterpret_cast<uint32_t*>(ws + o_idx);
+  uint32_t* sr_idx2 = reinterpret_cast<uint32_t*>(ws + o_idx2);
+  uint32_t* sr_vals = reinterpret_cast<uint32_t*>(ws + o_sr);
+  cudaError_t err;
+
+  const int smax = (1 << (sb - 1)) - 1;
+  absmax_kernel<<<dim3(static_cast<unsigned>(B), 3), 512, 0, stream>>>(a->q, a->k, a->v, a->in_dtype, n, qb,
+                                                                       scales, smax);
+  count_launch();
+  quant_kernel<<<dim3(static_cast<unsigned>((B * qwords + 255) / 256), 3), 256, 0, stream>>>(
+      a->q, a->k, a->v, a->in_dtype, n, qb, scales, qkv, qwords, B);
+  count_launch();
+  alpha_kernel<<<static_cast<unsigned>((B + 127) / 128), 128, 0, stream>>>(scales, B, a->head_dim, alpha_s, alpha_m);
+  count_launch();
+
+  // mask -> SR-BCRS structure of the probability matrix (stride = plan tile k)
+  if ((err = launch_srbcrs_plan(a->mask->row_offsets, vrows, S, sr_begin, sr_end, sr_total, stream)) != cudaSuccess)
+    return err;
+  // column indices for the worst-case stored count; padding tail stays sentinel
+  cudaMemsetAsync(sr_idx, 0xFF, max_stored * 4, stream);
+  if ((err = launch_srbcrs_fill(a->mask->row_offsets, a->mask->col_indices, vrows, nblk, 8, S, sr_begin, sr_end,
+                                max_stored, nullptr, 32, sr_idx, nullptr, stream)) != cudaSuccess)
+    return err;
+  const uint32_t* spmm_idx = sr_idx;
+  if (qb == 4) {  // attention.py:166-167
+    if ((err = launch_shuffle(sr_idx, max_stored, sr_idx2, stream)) != cudaSuccess) return err;
+    spmm_idx = sr_idx2;
+  }
+
+  SddmmParams sp{};
+  sp.M = L; sp.K = d; sp.N = L; sp.vrows = vrows; sp.n_blocks = nblk;
+  sp.V = 8; sp.LB = qb; sp.RB = qb; sp.batch = static_cast<int>(B);
+  sp.a_words = qkv; sp.a_stride = qwords;
+  sp.b_words = qkv + B * qwords; sp.b_stride = qwords;
+  sp.row_offsets = a->mask->row_offsets; sp.col_indices = a->mask->col_indices;
+  sp.out = a->scores_int; sp.out_stride = nblk * 8;
+  sp.alpha = alpha_s; sp.out_f16 = scores; sp.f16_stride = nblk * 8;
+  sp.status = status;
+  if ((err = launch_sddmm(sp, stream)) != cudaSuccess) return err;
+
+  const int64_t warps = B * vrows;
+  const unsigned grid = static_cast<unsigned>((warps * 32 + 255) / 256);
+  if (a->mode == MC_ATTN_FAST)
+    softmax_requant_kernel<true><<<grid, 256, 0, stream>>>(scores, nblk * 8, a->mask->row_offsets, vrows, sr_begin, S,
+                                                           smax, sb, sr_vals, sr_words, a->probs_f16, a->probs_int, B);
+  else
+    softmax_requant_kernel<false><<<grid, 256, 0, stream>>>(scores, nblk * 8, a->mask->row_offsets, vrows, sr_begin, S,
+                                                            smax, sb, sr_vals, sr_words, a->probs_f16, a->probs_int, B);
+  count_launch();
+
+  SpmmParams mp{};
+  mp.M = L; mp.K = L; mp.N = d; mp.vrows = vrows;
+  mp.V = 8; mp.S = S; mp.LB = sb; mp.RB = qb; mp.shuffled = qb == 4 ? 1 : 0; mp.batch = static_cast<int>(B);
+  mp.row_begin = sr_begin; mp.row_end = sr_end; mp.col_indices = spmm_idx;
+  mp.lhs_words = sr_vals; mp.lhs_stride = sr_words;
+  mp.rhs_words = qkv + 2 * B * qwords; mp.rhs_stride = qwords;
+  mp.out = a->mix_int; mp.out_stride = L * d;
+  mp.alpha = alpha_m; mp.out_f16 = a->out_f16; mp.f16_stride = L * d;
+  mp.status = status;
+  return launch_spmm(mp, stream);
+}
+
+}  // namespace mcube

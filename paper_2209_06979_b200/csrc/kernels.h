@@ -1,0 +1,66 @@
+// kernels.h -- internal launch interfaces shared by the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mcube {
+
+void count_launch();
+
+struct SpmmParams {
+  int64_t M, K, N, vrows;
+  int V, S, LB, RB, shuffled, batch;
+  const int64_t* row_begin;
+  const int64_t* row_end;
+  const uint32_t* col_indices;
+  const uint32_t* lhs_words;
+  int64_t lhs_stride;  // words per batch item
+  const uint32_t* rhs_words;
+  int64_t rhs_stride;
+  int32_t* out;
+  int64_t out_stride;
+  const double* alpha;
+  double alpha_host;
+  uint16_t* out_f16;
+  int64_t f16_stride;
+  uint32_t* status;
+  // filled by the launcher
+  int64_t ntiles, tasks;
+};
+
+struct SddmmParams {
+  int64_t M, K, N, vrows, n_blocks;
+  int V, LB, RB, batch;
+  const uint32_t* a_words;  // M x K row-major
+  int64_t a_stride;
+  const uint32_t* b_words;  // K x N column-major == N x K row-major
+  int64_t b_stride;
+  const int64_t* row_offsets;
+  const uint32_t* col_indices;
+  int32_t* out;
+  int64_t out_stride;
+  const double* alpha;
+  double alpha_host;
+  uint16_t* out_f16;
+  int64_t f16_stride;
+  uint32_t* status;
+  int splits;  // warps per vector row, chosen by the launcher
+  int64_t tasks;
+};
+
+cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream);
+cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream);
+
+// SR-BCRS packer (sparse_format.py:284-315)
+cudaError_t launch_srbcrs_plan(const int64_t* row_offsets, int64_t vrows, int stride,
+                               int64_t* row_begin, int64_t* row_end, int64_t* total,
+                               cudaStream_t stream);
+cudaError_t launch_srbcrs_fill(const int64_t* row_offsets, const uint32_t* col_indices,
+                               int64_t vrows, int64_t n_blocks, int V, int stride,
+                               const int64_t* row_begin, const int64_t* row_end,
+                               int64_t stored_total, const uint32_t* values, int bits,
+                               uint32_t* col_out, uint32_t* values_out, cudaStream_t stream);
+cudaError_t launch_shuffle(const uint32_t* in, int64_t n, uint32_t* out, cudaStream_t stream);
+
+}  // namespace mcube

@@ -1,0 +1,218 @@
+// sddmm.cu -- block-sampled dense x dense integer product (SDDMM) for B200.
+//
+// out[blk, v] = sum_k A[r*V + v, k] * B[k, c]   for each pattern block (r, c),
+// bit-exact with the reference kernels.sddmm (kernels.py:367-435).
+//
+// B is column-major, i.e. B^T is row-major with k contiguous, so both MMA
+// operands are already k-major: no transposes. Per warp task
+// (vector row r, a contiguous share of its blocks) 16 pattern blocks form the
+// MMA M dimension of mma.sync m16n8k32, the V rows of A the N dimension, and k
+// the reduction. 16/4-bit operands are split / sign-extended into int8 chunks
+// exactly as in spmm.cu; chunk products are recombined in int64 with the
+// reference's int32 checks (kernels.py:418-427).
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mcube {
+namespace {
+
+constexpr int kWarps = 4;
+
+// 16 consecutive k values of one operand row -> 4 int8-chunk words per chunk.
+template <int BITS, bool ALIGNED>
+__device__ __forceinline__ void load_k16(const uint32_t* __restrict__ words, int64_t row, int64_t K,
+                                         int64_t k0, bool row_ok, uint32_t (&w)[2][4]) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int x = 0; x < 4; ++x) w[c][x] = 0u;
+  if (!row_ok) return;
+  if constexpr (ALIGNED) {
+    const uint8_t* base = reinterpret_cast<const uint8_t*>(words) + (row * K * BITS) / 8;
+    if constexpr (BITS == 8) {
+      if (k0 < K) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(base + k0));
+        w[0][0] = u.x; w[0][1] = u.y; w[0][2] = u.z; w[0][3] = u.w;
+      }
+    } else if constexpr (BITS == 16) {
+      uint4 u0 = make_uint4(0, 0, 0, 0), u1 = make_uint4(0, 0, 0, 0);
+      if (k0 < K) u0 = __ldg(reinterpret_cast<const uint4*>(base + 2 * k0));
+      if (k0 + 8 < K) u1 = __ldg(reinterpret_cast<const uint4*>(base + 2 * k0 + 16));
+      split16(u0.x, u0.y, w[0][0], w[1][0]);
+      split16(u0.z, u0.w, w[0][1], w[1][1]);
+      split16(u1.x, u1.y, w[0][2], w[1][2]);
+      split16(u1.z, u1.w, w[0][3], w[1][3]);
+    } else {  // 4-bit
+      if (k0 < K) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(base + k0 / 2));
+        unpack_s4x8(u.x, w[0][0], w[0][1]);
+        unpack_s4x8(u.y, w[0][2], w[0][3]);
+      }
+    }
+  } else {
+    // generic path: element-wise, any K / alignment
+    int32_t e[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) e[i] = (k0 + i < K) ? fetch_packed(words, row * K + k0 + i, BITS) : 0;
+    auto pack4 = [](int32_t a, int32_t b, int32_t c, int32_t d) {
+      return (static_cast<uint32_t>(a) & 0xFF) | ((static_cast<uint32_t>(b) & 0xFF) << 8) |
+             ((static_cast<uint32_t>(c) & 0xFF) << 16) | ((static_cast<uint32_t>(d) & 0xFF) << 24);
+    };
+    if constexpr (BITS == 16) {
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        w[0][x] = pack4(e[4 * x], e[4 * x + 1], e[4 * x + 2], e[4 * x + 3]);
+        w[1][x] = pack4(e[4 * x] >> 8, e[4 * x + 1] >> 8, e[4 * x + 2] >> 8, e[4 * x + 3] >> 8);
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < 4; ++x) w[0][x] = pack4(e[4 * x], e[4 * x + 1], e[4 * x + 2], e[4 * x + 3]);
+    }
+  }
+}
+
+template <int LB, int RB, int V, bool ALIGNED>
+__global__ void __launch_bounds__(kWarps * 32)
+sddmm_kernel(const SddmmParams p) {
+  constexpr int LC = (LB == 16) ? 2 : 1;
+  constexpr int RC = (RB == 16) ? 2 : 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t task = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  if (task >= p.tasks) return;
+  const int64_t per_batch = p.vrows * p.splits;
+  const int64_t b = task / per_batch;
+  const int64_t rem = task - b * per_batch;
+  const int64_t r = rem / p.splits;
+  const int split = static_cast<int>(rem - r * p.splits);
+  const int64_t lo = p.row_offsets[r], hi = p.row_offsets[r + 1];
+  const int64_t nb = hi - lo;
+  const int64_t ngroups = (nb + 15) >> 4;
+  const int64_t gbeg = (ngroups * split) / p.splits, gend = (ngroups * (split + 1)) / p.splits;
+  const uint32_t* __restrict__ A = p.a_words + b * p.a_stride;
+  const uint32_t* __restrict__ Bt = p.b_words + b * p.b_stride;
+  const int64_t arow = r * V + g;
+  const bool a_ok = g < V;
+  double alpha = 0.0;
+  if (p.out_f16) alpha = p.alpha ? p.alpha[b] : p.alpha_host;
+  bool overflow = false;
+
+  for (int64_t gi = gbeg; gi < gend; ++gi) {
+    const int64_t blk0 = lo + gi * 16;
+    const int nvalid = static_cast<int>(min_i64(16, hi - blk0));
+    uint32_t mycol = (lane < nvalid) ? __ldg(p.col_indices + blk0 + lane) : 0u;
+    if (lane < nvalid && mycol >= static_cast<uint32_t>(p.N)) {
+      flag_status(p.status, MC_STATUS_BAD_INDEX);
+      mycol = 0u;
+    }
+    const uint32_t c_lo = __shfl_sync(0xffffffffu, mycol, g);
+    const uint32_t c_hi = __shfl_sync(0xffffffffu, mycol, g + 8);
+    const bool lo_ok = g < nvalid, hi_ok = g + 8 < nvalid;
+
+    int acc[LC][RC][4];
+#pragma unroll
+    for (int c = 0; c < LC; ++c)
+#pragma unroll
+      for (int j = 0; j < RC; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[c][j][e] = 0;
+
+    for (int64_t ks = 0; ks < p.K; ks += 64) {
+      const int64_t k0 = ks + 16 * t;
+      uint32_t wa[2][4], wl[2][4], wh[2][4];
+      load_k16<LB, ALIGNED>(A, arow, p.K, k0, a_ok, wa);
+      load_k16<RB, ALIGNED>(Bt, c_lo, p.K, k0, lo_ok, wl);
+      load_k16<RB, ALIGNED>(Bt, c_hi, p.K, k0, hi_ok, wh);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+#pragma unroll
+          for (int c = 0; c < LC; ++c) {
+            const uint32_t a0 = wl[j][2 * half], a2 = wl[j][2 * half + 1];
+            const uint32_t a1 = wh[j][2 * half], a3 = wh[j][2 * half + 1];
+            const uint32_t b0 = wa[c][2 * half], b1 = wa[c][2 * half + 1];
+            const bool au = (RB == 16) && (j == 0);
+            const bool bu = (LB == 16) && (c == 0);
+            if (au && bu) mma16832<true, true>(acc[c][j], a0, a1, a2, a3, b0, b1);
+            else if (au) mma16832<true, false>(acc[c][j], a0, a1, a2, a3, b0, b1);
+            else if (bu) mma16832<false, true>(acc[c][j], a0, a1, a2, a3, b0, b1);
+            else mma16832<false, false>(acc[c][j], a0, a1, a2, a3, b0, b1);
+          }
+        }
+      }
+    }
+
+    // epilogue: D[m = block, n = v]; c0:(g,2t) c1:(g,2t+1) c2:(g+8,2t) c3:(g+8,2t+1)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int m = (e < 2) ? g : g + 8;
+      const int v = 2 * t + (e & 1);
+      long long total = 0;
+#pragma unroll
+      for (int j = 0; j < RC; ++j) {
+        long long tj;
+        if constexpr (LC == 2) {
+          const long long lo_p = acc[0][j][e];
+          const long long hi_p = 256LL * acc[1][j][e];
+          if constexpr (V == 8) overflow |= !fits_i32(hi_p);
+          else overflow |= !fits_i32(lo_p + hi_p);
+          tj = lo_p + hi_p;
+        } else {
+          tj = acc[0][j][e];
+        }
+        total += tj << (8 * j);
+      }
+      if (m < nvalid && v < V) {
+        overflow |= !fits_i32(total);
+        const int64_t o = (blk0 + m) * V + v;
+        if (p.out) p.out[b * p.out_stride + o] = static_cast<int32_t>(total);
+        if (p.out_f16) p.out_f16[b * p.f16_stride + o] = f16_bits_rn(static_cast<double>(total) * alpha);
+      }
+    }
+  }
+  if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
+}
+
+template <int LB, int RB, int V>
+cudaError_t launch_v(const SddmmParams& p, cudaStream_t s) {
+  const bool aligned = ((p.K * LB / 8) % 16 == 0) && ((p.K * RB / 8) % 16 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(p.a_words) & 15) == 0) &&
+                       ((reinterpret_cast<uintptr_t>(p.b_words) & 15) == 0) &&
+                       ((p.a_stride * 4) % 16 == 0) && ((p.b_stride * 4) % 16 == 0);
+  const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
+  if (grid == 0) return cudaSuccess;
+  if (aligned) sddmm_kernel<LB, RB, V, true><<<grid, kWarps * 32, 0, s>>>(p);
+  else sddmm_kernel<LB, RB, V, false><<<grid, kWarps * 32, 0, s>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int LB, int RB>
+cudaError_t launch_lr(const SddmmParams& p, cudaStream_t s) {
+  switch (p.V) {
+    case 2: return launch_v<LB, RB, 2>(p, s);
+    case 4: return launch_v<LB, RB, 4>(p, s);
+    default: return launch_v<LB, RB, 8>(p, s);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream) {
+  // warps per vector row: about 4 groups of 16 blocks each
+  const double avg_groups = p.vrows ? (static_cast<double>(p.n_blocks) / p.vrows) / 16.0 : 0.0;
+  int splits = static_cast<int>(avg_groups / 4.0);
+  p.splits = splits < 1 ? 1 : (splits > 64 ? 64 : splits);
+  p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.splits;
+  switch (p.LB * 100 + p.RB) {
+    case 1616: return launch_lr<16, 16>(p, stream);
+    case 808: return launch_lr<8, 8>(p, stream);
+    case 404: return launch_lr<4, 4>(p, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mcube

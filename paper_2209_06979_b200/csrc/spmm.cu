@@ -1,0 +1,421 @@
+// spmm.cu -- SR-BCRS x dense integer SpMM for B200 (sm_100a).
+//
+// Computes out[M x N] = A (SR-BCRS, L-bit, vector length V) x B (K x N row-major,
+// R-bit), bit-exact with the reference kernels.spmm (kernels.py:293-340).
+//
+// Formulation (transposed, B200 view of PAPER.md §4.2): per vector row r and a
+// 64-column tile, D^T[n, v] = sum_k B[idx_k, n] * A_r[v, k], so dense columns are
+// the MMA M dimension (16 per mma.sync m16n8k32), the V rows are MMA N (8) and the
+// gathered k is MMA K (32). Every operand chunk is int8 (s8/u8): 16-bit operands
+// split into (u8 low byte, s8 high byte) chunks, 4-bit operands are sign-extended
+// to s8, 12-bit LHS values split like 16-bit ones (qint.py:209-225). Chunk products
+// live in separate exact int32 accumulators and are recombined with shift-add in
+// the epilogue, where the reference's int32 checks (kernels.py:286-288,
+// tile_engine.py:246-247) are evaluated exactly in int64.
+//
+// Data movement (the Alg. 1 prefetch pipeline of PAPER.md:272-301, kernels.py:343-364):
+// each warp owns a (row, 64-column tile) task and runs a STAGES-deep cp.async ring:
+// stage s holds the 32 gathered B-row segments of k-step s (zero-filled for
+// sentinel/padding slots, kernels.py:224-236) plus the matching 2 x V x 16 LHS
+// values. The gathered rows are stored in a slot order and XOR swizzle that makes
+// the consumer's shared-memory reads bank-conflict free for any column indices.
+// Consumers transpose 4x4 byte blocks with PRMT into the k-major
+// MMA fragments. Column indices for the next issue are prefetched one step ahead.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace mcube {
+
+namespace {
+
+constexpr int kWarps = 4;
+constexpr int kStages = 4;
+constexpr int kTileN = 64;
+
+template <int LB, int RB, int V>
+struct SpmmCfg {
+  static constexpr int LC = (LB >= 12) ? 2 : 1;        // LHS int8 chunks
+  static constexpr int RC = (RB == 16) ? 2 : 1;        // RHS int8 chunks
+  static constexpr int RBYTES = kTileN * RB / 8;       // bytes of one gathered row segment
+  static constexpr int CPR = RBYTES / 16;              // 16-byte copies per row segment
+  static constexpr int ABYTES = 2 * LB;                // bytes of 16 LHS values
+  static constexpr int B_STAGE = 32 * RBYTES;
+  static constexpr int A_STAGE = 2 * V * ABYTES;
+  static constexpr int STAGE = B_STAGE + A_STAGE;
+  static constexpr int A_COPIES = A_STAGE / 8;         // 8-byte copies
+};
+
+__device__ __forceinline__ int slot_of(int kk) {
+  return ((kk >> 4) << 4) | ((kk & 3) << 2) | ((kk >> 2) & 3);
+}
+
+template <int RBYTES>
+__device__ __forceinline__ int swz(int t) {
+  if constexpr (RBYTES == 128) return 32 * t;
+  if constexpr (RBYTES == 64) return 32 * (t >> 1);
+  return 0;
+}
+
+// value position -> stored index position (SHUFFLE_PERMUTATION inverse, sparse_format.py:222-230)
+__device__ __forceinline__ int64_t idx_pos(int64_t q, bool shuffled) {
+  if (!shuffled) return q;
+  const int w = static_cast<int>(q & 7);
+  return (q & ~7LL) | ((w >> 1) | ((w & 1) << 2));
+}
+
+template <int LB, int RB, int V, bool ALIGNED>
+__global__ void __launch_bounds__(kWarps * 32)
+spmm_kernel(const SpmmParams p) {
+  using C = SpmmCfg<LB, RB, V>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t task = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  if (task >= p.tasks) return;
+  const int64_t per_batch = p.vrows * p.ntiles;
+  const int64_t b = task / per_batch;
+  const int64_t rem = task - b * per_batch;
+  const int64_t r = rem / p.ntiles;
+  const int64_t c0 = (rem - r * p.ntiles) * kTileN;
+
+  const uint32_t* __restrict__ lhs = p.lhs_words + b * p.lhs_stride;
+  const uint32_t* __restrict__ rhs = p.rhs_words + b * p.rhs_stride;
+  const int64_t p_begin = p.row_begin[r];
+  const int64_t n_true = p.row_end[r] - p_begin;
+  const int64_t stored = ((n_true + p.S - 1) / p.S) * p.S;
+  const int64_t p_end = p_begin + stored;
+  const int nsteps = static_cast<int>((stored + 31) >> 5);
+  const bool shuffled = p.shuffled != 0;
+
+  uint8_t* wbuf = smem + warp * (kStages * C::STAGE);
+  const uint32_t wbuf_s = smem_u32(wbuf);
+
+  // ---- producer state: column indices for this lane's copies, one step ahead ----
+  uint32_t nidx[C::CPR];
+  auto load_idx = [&](int step) {
+#pragma unroll
+    for (int u = 0; u < C::CPR; ++u) {
+      const int kk = (lane + 32 * u) / C::CPR;
+      const int64_t q = p_begin + 32LL * step + kk;
+      nidx[u] = (q < p_end) ? __ldg(p.col_indices + idx_pos(q, shuffled)) : kSentinel;
+    }
+  };
+
+  auto issue = [&](int step) {
+    const uint32_t sbase = wbuf_s + (step % kStages) * C::STAGE;
+#pragma unroll
+    for (int u = 0; u < C::CPR; ++u) {
+      const int q = lane + 32 * u;
+      const int kk = q / C::CPR;
+      const int ch = q % C::CPR;
+      const int slot = slot_of(kk);
+      const uint32_t dst = sbase + slot * C::RBYTES + ((ch * 16) ^ swz<C::RBYTES>(slot & 3));
+      uint32_t col = nidx[u];
+      bool ok = col != kSentinel;
+      if (ok && col >= static_cast<uint32_t>(p.K)) {
+        flag_status(p.status, MC_STATUS_BAD_INDEX);
+        ok = false;
+      }
+      if constexpr (ALIGNED) {
+        const int64_t rem_bytes = ((p.N - c0) * RB) / 8 - ch * 16;
+        const uint32_t nbytes = (ok && rem_bytes > 0) ? 16u : 0u;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(rhs);
+        if (nbytes) src += ((static_cast<int64_t>(col) * p.N + c0) * RB) / 8 + ch * 16;
+        cp_async16(dst, src, nbytes);
+      } else {
+        // generic path: element-wise fetch for rows that are not 16-byte aligned
+        constexpr int EPC = 128 / RB;  // elements per 16-byte chunk
+        uint32_t wv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const int64_t n = c0 + ch * EPC + e;
+          uint32_t x = 0;
+          if (ok && n < p.N)
+            x = static_cast<uint32_t>(fetch_packed(rhs, static_cast<int64_t>(col) * p.N + n, RB)) &
+                ((1u << RB) - 1u);
+          const int bit = e * RB;
+          wv[bit >> 5] |= x << (bit & 31);
+        }
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(dst), "r"(wv[0]), "r"(wv[1]),
+                     "r"(wv[2]), "r"(wv[3]));
+      }
+    }
+    // LHS values of this step: 2 halves x V rows x 16 elements, 8-byte copies
+    const uint32_t abase = sbase + C::B_STAGE;
+#pragma unroll
+    for (int u = 0; u < (C::A_COPIES + 31) / 32; ++u) {
+      const int q = lane + 32 * u;
+      if (q < C::A_COPIES) {
+        const int per_row = C::ABYTES / 8;
+        const int row = q / per_row;  // row = h*V + v
+        const int part = q % per_row;
+        const int h = row / V, v = row % V;
+        const int64_t pos = p_begin + 32LL * step + 16 * h;
+        const bool ok = pos < p_end;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(lhs);
+        if (ok) {
+          const int64_t e = (pos / p.S) * V * p.S + static_cast<int64_t>(v) * p.S + (pos % p.S);
+          src += (e * LB) / 8 + part * 8;
+        }
+        cp_async8(abase + row * C::ABYTES + part * 8, src, ok ? 8u : 0u);
+      }
+    }
+  };
+
+  int acc[C::LC][C::RC][4][4];
+#pragma unroll
+  for (int c = 0; c < C::LC; ++c)
+#pragma unroll
+    for (int j = 0; j < C::RC; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[c][j][q][e] = 0;
+
+  if (nsteps > 0) {
+    load_idx(0);
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) {
+      if (s < nsteps) {
+        issue(s);
+        if (s + 1 < nsteps) load_idx(s + 1);
+      }
+      cp_async_commit();
+    }
+  }
+
+  for (int s = 0; s < nsteps; ++s) {
+    const int nxt = s + kStages - 1;
+    if (nxt < nsteps) {
+      issue(nxt);
+      if (nxt + 1 < nsteps) load_idx(nxt + 1);
+    }
+    cp_async_commit();
+    cp_async_wait<kStages - 1>();
+    __syncwarp();
+
+    const uint8_t* sb = wbuf + (s % kStages) * C::STAGE;
+    const uint8_t* sa = sb + C::B_STAGE;
+
+    // ---- MMA B operand: LHS chunk words for kk = 16h + 4t .. +3 of row v = g ----
+    uint32_t bf[C::LC][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint8_t* ar = sa + (h * V + (g < V ? g : 0)) * C::ABYTES;
+      if constexpr (LB == 8) {
+        bf[0][h] = *reinterpret_cast<const uint32_t*>(ar + 4 * t);
+      } else if constexpr (LB == 4) {
+        bf[0][h] = unpack_s4x4_ordered(*reinterpret_cast<const uint16_t*>(ar + 2 * t));
+      } else if constexpr (LB == 16) {
+        const uint2 w = *reinterpret_cast<const uint2*>(ar + 8 * t);
+        split16(w.x, w.y, bf[0][h], bf[1][h]);
+      } else {  // LB == 12: 4 elements = 48 bits starting at bit 48t
+        const uint32_t* aw = reinterpret_cast<const uint32_t*>(ar);
+        const int w0 = (3 * t) >> 1;
+        const uint64_t bits = (static_cast<uint64_t>(aw[w0]) | (static_cast<uint64_t>(aw[w0 + 1]) << 32)) >>
+                              (16 * (t & 1));
+        uint32_t e0 = static_cast<uint32_t>(bits) & 0xFFFu, e1 = static_cast<uint32_t>(bits >> 12) & 0xFFFu;
+        uint32_t e2 = static_cast<uint32_t>(bits >> 24) & 0xFFFu, e3 = static_cast<uint32_t>(bits >> 36) & 0xFFFu;
+        // low byte (unsigned chunk), high nibble sign-extended (signed chunk)
+        bf[0][h] = (e0 & 0xFF) | ((e1 & 0xFF) << 8) | ((e2 & 0xFF) << 16) | ((e3 & 0xFF) << 24);
+        bf[1][h] = sext_nibble_bytes((e0 >> 8) | ((e1 >> 8) << 8) | ((e2 >> 8) << 16) | ((e3 >> 8) << 24));
+      }
+      if (g >= V) {
+#pragma unroll
+        for (int c = 0; c < C::LC; ++c) bf[c][h] = 0u;
+      }
+    }
+
+    // ---- MMA A operand: gathered rows, transposed to k-major words per column ----
+    uint32_t T[C::RC][2][8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t raw[4][RB / 4 > 0 ? RB / 4 : 1];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int slot = 16 * h + 4 * i + t;
+        const uint8_t* rp = sb + slot * C::RBYTES + ((g * RB) ^ swz<C::RBYTES>(t));
+        if constexpr (RB == 8) {
+          const uint2 w = *reinterpret_cast<const uint2*>(rp);
+          raw[i][0] = w.x;
+          raw[i][1] = w.y;
+        } else if constexpr (RB == 16) {
+          const uint4 w = *reinterpret_cast<const uint4*>(rp);
+          raw[i][0] = w.x;
+          raw[i][1] = w.y;
+          raw[i][2] = w.z;
+          raw[i][3] = w.w;
+        } else {
+          raw[i][0] = *reinterpret_cast<const uint32_t*>(rp);
+        }
+      }
+      if constexpr (RB == 8) {
+        transpose4x4(raw[0][0], raw[1][0], raw[2][0], raw[3][0], T[0][h][0], T[0][h][1], T[0][h][2], T[0][h][3]);
+        transpose4x4(raw[0][1], raw[1][1], raw[2][1], raw[3][1], T[0][h][4], T[0][h][5], T[0][h][6], T[0][h][7]);
+      } else if constexpr (RB == 16) {
+        uint32_t lo0[4], lo1[4], hi0[4], hi1[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          split16(raw[i][0], raw[i][1], lo0[i], hi0[i]);
+          split16(raw[i][2], raw[i][3], lo1[i], hi1[i]);
+        }
+        transpose4x4(lo0[0], lo0[1], lo0[2], lo0[3], T[0][h][0], T[0][h][1], T[0][h][2], T[0][h][3]);
+        transpose4x4(lo1[0], lo1[1], lo1[2], lo1[3], T[0][h][4], T[0][h][5], T[0][h][6], T[0][h][7]);
+        transpose4x4(hi0[0], hi0[1], hi0[2], hi0[3], T[1][h][0], T[1][h][1], T[1][h][2], T[1][h][3]);
+        transpose4x4(hi1[0], hi1[1], hi1[2], hi1[3], T[1][h][4], T[1][h][5], T[1][h][6], T[1][h][7]);
+      } else {
+        uint32_t ev[4], od[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) unpack_s4x8(raw[i][0], ev[i], od[i]);
+        // even columns 0,2,4,6 -> T[0..3]; odd columns 1,3,5,7 -> T[4..7]
+        transpose4x4(ev[0], ev[1], ev[2], ev[3], T[0][h][0], T[0][h][1], T[0][h][2], T[0][h][3]);
+        transpose4x4(od[0], od[1], od[2], od[3], T[0][h][4], T[0][h][5], T[0][h][6], T[0][h][7]);
+      }
+    }
+
+#pragma unroll
+    for (int j = 0; j < C::RC; ++j) {
+      constexpr bool kDummy = false;
+      (void)kDummy;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        // m = g <-> column 8g + 2q, m = g + 8 <-> column 8g + 2q + 1
+        const int x0 = (RB == 4) ? q : 2 * q;
+        const int x1 = (RB == 4) ? 4 + q : 2 * q + 1;
+        const uint32_t a0 = T[j][0][x0], a1 = T[j][0][x1];
+        const uint32_t a2 = T[j][1][x0], a3 = T[j][1][x1];
+#pragma unroll
+        for (int c = 0; c < C::LC; ++c) {
+          const bool au = (RB == 16) && (j == 0);
+          const bool bu = (LB >= 12) && (c == 0);
+          if (au && bu) mma16832<true, true>(acc[c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
+          else if (au) mma16832<true, false>(acc[c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
+          else if (bu) mma16832<false, true>(acc[c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
+          else mma16832<false, false>(acc[c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();
+
+  // ---- epilogue: exact shift-add recombination + the reference's int32 checks ----
+  bool overflow = false;
+  int32_t vals[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      long long total = 0;
+#pragma unroll
+      for (int j = 0; j < C::RC; ++j) {
+        long long tj;
+        if constexpr (C::LC == 2) {
+          const long long lo = acc[0][j][q][e];
+          const long long hi = 256LL * acc[1][j][q][e];
+          constexpr bool w8 = (RB != 4);
+          if constexpr (w8) {
+            if constexpr (V == 8) overflow |= !fits_i32(hi);
+            else overflow |= !fits_i32(lo + hi);
+          } else {
+            if constexpr (V == 4) overflow |= !fits_i32(hi);
+          }
+          tj = lo + hi;
+        } else {
+          tj = acc[0][j][q][e];
+        }
+        total += tj << (8 * j);
+      }
+      overflow |= !fits_i32(total);
+      vals[q][e] = static_cast<int32_t>(total);
+    }
+  }
+  if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
+
+  double alpha = 0.0;
+  if (p.out_f16) alpha = p.alpha ? p.alpha[b] : p.alpha_host;
+  const int64_t row0 = r * V;
+#pragma unroll
+  for (int vv = 0; vv < 2; ++vv) {
+    const int v = 2 * t + vv;
+    if (v >= V) continue;
+    int32_t rowv[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      rowv[2 * q] = vals[q][vv];
+      rowv[2 * q + 1] = vals[q][2 + vv];
+    }
+    const int64_t n0 = c0 + 8 * g;
+    const int64_t base = (row0 + v) * p.N + n0;
+    if (p.out) {
+      int32_t* o = p.out + b * p.out_stride + base;
+      if (n0 + 8 <= p.N && (p.N & 3) == 0) {
+        reinterpret_cast<int4*>(o)[0] = make_int4(rowv[0], rowv[1], rowv[2], rowv[3]);
+        reinterpret_cast<int4*>(o)[1] = make_int4(rowv[4], rowv[5], rowv[6], rowv[7]);
+      } else {
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          if (n0 + x < p.N) o[x] = rowv[x];
+      }
+    }
+    if (p.out_f16) {
+      uint16_t* o = p.out_f16 + b * p.f16_stride + base;
+#pragma unroll
+      for (int x = 0; x < 8; ++x)
+        if (n0 + x < p.N) o[x] = f16_bits_rn(static_cast<double>(rowv[x]) * alpha);
+    }
+  }
+}
+
+template <int LB, int RB, int V>
+cudaError_t launch_spmm_v(const SpmmParams& p, cudaStream_t stream) {
+  using C = SpmmCfg<LB, RB, V>;
+  const int smem = kWarps * kStages * C::STAGE;
+  const bool aligned = ((p.N * RB / 8) % 16 == 0) && ((reinterpret_cast<uintptr_t>(p.rhs_words) & 15) == 0) &&
+                       ((p.rhs_stride * 4) % 16 == 0);
+  const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
+  if (grid == 0) return cudaSuccess;
+  if (aligned) {
+    auto k = spmm_kernel<LB, RB, V, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k<<<grid, kWarps * 32, smem, stream>>>(p);
+  } else {
+    auto k = spmm_kernel<LB, RB, V, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k<<<grid, kWarps * 32, smem, stream>>>(p);
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int LB, int RB>
+cudaError_t launch_spmm_lr(const SpmmParams& p, cudaStream_t stream) {
+  switch (p.V) {
+    case 2: return launch_spmm_v<LB, RB, 2>(p, stream);
+    case 4: return launch_spmm_v<LB, RB, 4>(p, stream);
+    default: return launch_spmm_v<LB, RB, 8>(p, stream);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream) {
+  p.ntiles = (p.N + kTileN - 1) / kTileN;
+  p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.ntiles;
+  const int key = p.LB * 100 + p.RB;
+  switch (key) {
+    case 1616: return launch_spmm_lr<16, 16>(p, stream);
+    case 1608: return launch_spmm_lr<16, 8>(p, stream);
+    case 1604: return launch_spmm_lr<16, 4>(p, stream);
+    case 1204: return launch_spmm_lr<12, 4>(p, stream);
+    case 804: return launch_spmm_lr<8, 4>(p, stream);
+    case 808: return launch_spmm_lr<8, 8>(p, stream);
+    case 404: return launch_spmm_lr<4, 4>(p, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace mcube

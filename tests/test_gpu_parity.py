@@ -1,0 +1,235 @@
+"""Device parity: CUDA path (through the C ABI) vs the reference's golden vectors and the oracle.
+
+Integer results must be bit-exact; attention parity mode must reproduce the
+reference's integer stages and fp16 output exactly; fast mode is checked
+against the stated tolerance (max-abs 1e-3 on the fp16 output).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import cuda_available, golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+if cuda_available():
+    import torch
+    import paper_2209_06979_b200 as mc
+    from paper_2209_06979_b200.qint import COL_MAJOR, ROW_MAJOR
+
+SPMM = load_golden("spmm")
+SDDMM = load_golden("sddmm")
+ATT = load_golden("attention")
+FMT = load_golden("formats")
+
+
+def _srbcrs_from_golden(g, prefix, device=False):
+    rows, cols, v, stride, bits, shuffled = [int(x) for x in g[prefix + "meta"]]
+    begin, end = g[prefix + "row_begin"], g[prefix + "row_end"]
+    idx, words = g[prefix + "col_indices"], g[prefix + "words"]
+    count = idx.size * v
+    if device:
+        begin, end = torch.from_numpy(begin).cuda(), torch.from_numpy(end).cuda()
+        idx = torch.from_numpy(idx.view(np.int32)).cuda()
+        words = torch.from_numpy(words.view(np.int32)).cuda()
+    return mc.SrBcrsMatrix(rows, cols, v, stride, begin, end, idx,
+                           mc.PackedArray(count, bits, True, words), shuffled=bool(shuffled))
+
+
+@pytest.mark.parametrize("device", [False, True])
+@pytest.mark.parametrize("name", golden_cases(SPMM))
+def test_spmm_golden(name, device):
+    m, n, k, v, sp, lb, rb, seed, mult = [int(x) for x in SPMM[name + "/args"]]
+    lhs = _srbcrs_from_golden(SPMM, name + "/lhs_", device)
+    words = SPMM[name + "/rhs_words"]
+    if device:
+        words = torch.from_numpy(words.view(np.int32)).cuda()
+    rhs = mc.PackedMatrix(k, n, rb, ROW_MAJOR, True, words)
+    out = mc.spmm(mc.SpmmProblem(lhs, rhs))
+    if device:
+        assert out.is_cuda and out.dtype == torch.int32
+        out = out.cpu().numpy()
+    assert out.dtype == np.int32
+    assert (out == SPMM[name + "/out"]).all()
+
+
+@pytest.mark.parametrize("name", ["pair_8_8_v8", "pair_16_4_v4"])
+def test_spmm_pipelined_trace(name):
+    lhs = _srbcrs_from_golden(SPMM, name + "/lhs_")
+    m, n, k, v, sp, lb, rb, seed, mult = [int(x) for x in SPMM[name + "/args"]]
+    rhs = mc.PackedMatrix(k, n, rb, ROW_MAJOR, True, SPMM[name + "/rhs_words"])
+    out, traces = mc.spmm_pipelined(mc.SpmmProblem(lhs, rhs, mc.TilingConfig(pipeline=True)))
+    assert (out == SPMM[name + "/out"]).all()
+    steps = lhs.stored_count(0) // mc.plan(lb, rb).tile.k
+    assert traces[0][1] == mc.alg1_trace(steps)
+
+
+def test_spmm_epilogue_hook():
+    name = "pair_8_8_v8"
+    lhs = _srbcrs_from_golden(SPMM, name + "/lhs_")
+    rhs = mc.PackedMatrix(128, 64, 8, ROW_MAJOR, True, SPMM[name + "/rhs_words"])
+    out = mc.spmm(mc.SpmmProblem(lhs, rhs, epilogue=lambda acc: acc.astype(np.float64) * 0.5))
+    assert out.dtype == np.float64
+    assert (out == SPMM[name + "/out"] * 0.5).all()
+
+
+@pytest.mark.parametrize("name", golden_cases(SDDMM))
+def test_sddmm_golden(name):
+    m, n, k, v, sp, lb, rb, seed, fmt = [int(x) for x in SDDMM[name + "/args"]]
+    offs, cols = SDDMM[name + "/pattern_offsets"], SDDMM[name + "/pattern_cols"]
+    pattern = mc.BcrsMatrix(m, n, v, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * v), 8))
+    a = mc.PackedMatrix(m, k, lb, ROW_MAJOR, True, SDDMM[name + "/a_words"])
+    b = mc.PackedMatrix(k, n, rb, COL_MAJOR, True, SDDMM[name + "/b_words"])
+    out = mc.sddmm(mc.SddmmProblem(a, b, pattern, out_format="sr-bcrs" if fmt else "bcrs"))
+    if fmt:
+        assert isinstance(out, mc.SrBcrsMatrix) and out.stride == int(SDDMM[name + "/out_stride"][0])
+        assert (out.col_indices == SDDMM[name + "/out_col_indices"]).all()
+        assert (out.row_begin == SDDMM[name + "/out_row_begin"]).all()
+    assert (np.asarray(out.values) == SDDMM[name + "/out_values"]).all()
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_device_packer_and_shuffle(case):
+    p = f"gen{case}/"
+    rows, cols, v, sp, seed, bw, stride = [int(x) for x in FMT[p + "args"]]
+    b = mc.BcrsMatrix(rows, cols, v, FMT[p + "offsets"], FMT[p + "cols"],
+                      mc.PackedArray(FMT[p + "cols"].size * v, bw, True, FMT[p + "words"]))
+    s = mc.bcrs_to_srbcrs(b, stride)
+    assert (s.row_begin == FMT[p + "sr_row_begin"]).all()
+    assert (s.row_end == FMT[p + "sr_row_end"]).all()
+    assert (s.col_indices == FMT[p + "sr_col_indices"]).all()
+    assert (s.values.words == FMT[p + "sr_words"]).all()
+    if p + "shuffled_cols" in FMT.files:
+        sh = mc.shuffle_indices(s)
+        assert sh.shuffled and (sh.col_indices == FMT[p + "shuffled_cols"]).all()
+        with pytest.raises(mc.ShuffleStateError):
+            mc.shuffle_indices(sh)
+
+
+def test_packer_hand_layout_and_generator():
+    d = FMT["hand_dense"]
+    s = mc.bcrs_to_srbcrs(mc.dense_to_bcrs(d, 2), 4)
+    assert list(s._flat_values) == [1, 3, 5, 0, 2, 4, 6, 0]
+    assert (s.col_indices == FMT["hand_col_indices"]).all()
+    assert (mc.srbcrs_to_dense(s) == d).all()
+
+
+@pytest.mark.parametrize("name", golden_cases(ATT))
+def test_attention_parity_golden(name):
+    L, sb, qb, d, seed = [int(x) for x in ATT[name + "/args"]]
+    offs, cols = ATT[name + "/mask_offsets"], ATT[name + "/mask_cols"]
+    mask = mc.BcrsMatrix(L, L, 8, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * 8), 8))
+    cfg = mc.AttentionConfig(L, sb, qb, mask, head_dim=d)
+    q, k, v = (ATT[name + "/" + x].astype(np.float64) for x in "qkv")
+    res = mc.sparse_attention(q, k, v, cfg, mode="parity")
+    assert (res.scores_int == ATT[name + "/scores_int"]).all()
+    assert (res.probs_int._flat_values == ATT[name + "/probs_int"]).all()
+    assert (res.mix_int == ATT[name + "/mix_int"]).all()
+    assert (res.output.astype(np.float16) == ATT[name + "/output"]).all()
+    sc = ATT[name + "/scales"]
+    assert [res.params[x].scale for x in ("q", "k", "v", "softmax")] == list(sc)
+
+
+@pytest.mark.parametrize("name", ["att_8_8_90", "att_16_8_95", "att_8_4_90", "att_8_8_L256"])
+def test_attention_fast_mode_tolerance(name):
+    L, sb, qb, d, seed = [int(x) for x in ATT[name + "/args"]]
+    offs, cols = ATT[name + "/mask_offsets"], ATT[name + "/mask_cols"]
+    mask = mc.BcrsMatrix(L, L, 8, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * 8), 8))
+    cfg = mc.AttentionConfig(L, sb, qb, mask, head_dim=d)
+    q, k, v = (torch.from_numpy(ATT[name + "/" + x]).cuda() for x in "qkv")
+    out = mc.batched_sparse_attention(q[None], k[None], v[None], cfg, mode="fast")[0]
+    ref = ATT[name + "/output"].astype(np.float64)
+    err = np.abs(out.double().cpu().numpy() - ref).max()
+    assert err <= mc.attention.FAST_MODE_TOLERANCE, err
+
+
+def test_multi_head_equals_single_head():
+    a = O.build_attention_case(64, 16, 0.9, seed=11)
+    mask = mc.BcrsMatrix(64, 64, 8, a["offsets"], a["col_indices"],
+                         mc.PackedArray.from_values(np.ones(a["col_indices"].size * 8), 8))
+    cfg = mc.AttentionConfig(64, 8, 8, mask, head_dim=16, num_heads=3)
+    rng = np.random.default_rng(12)
+    q, k, v = (rng.normal(size=(3, 64, 16)) for _ in range(3))
+    out = mc.multi_head_attention(q, k, v, cfg)
+    single = mc.sparse_attention(q[1], k[1], v[1], cfg)
+    assert out.shape == (3, 64, 16)
+    assert (out[1] == single.output).all()
+
+
+# ---------------- randomized oracle sweeps (beyond the golden grid) ----------------
+
+PAIRS = [(16, 16), (16, 8), (16, 4), (12, 4), (8, 4), (8, 8), (4, 4)]
+
+
+@pytest.mark.parametrize("pair", PAIRS)
+@pytest.mark.parametrize("v", [2, 4, 8])
+@pytest.mark.parametrize("sparsity", [0.5, 0.9, 0.98])
+def test_spmm_random_vs_oracle(pair, v, sparsity):
+    lb, rb = pair
+    c = O.build_spmm_case(128, 192, 512, v, sparsity, lb, rb, seed=lb * 100 + rb * 10 + v)
+    lhs = mc.SrBcrsMatrix(128, 512, v, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                          mc.PackedArray.from_values(c["values"], lb), shuffled=c["shuffled"])
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], rb)))
+    want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], v, c["stride"],
+                  c["shuffled"], lb, c["rhs"], rb, 512)
+    assert (out == want).all()
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 100, 130])
+def test_spmm_unaligned_n_generic_path(n):
+    c = O.build_spmm_case(32, n, 96, 8, 0.7, 8, 4, seed=n)
+    lhs = mc.SrBcrsMatrix(32, 96, 8, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                          mc.PackedArray.from_values(c["values"], 8), shuffled=True)
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], 4)))
+    want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], 8, c["stride"], True,
+                  8, c["rhs"], 4, 96)
+    assert (out == want).all()
+
+
+@pytest.mark.parametrize("pair", [(16, 16), (8, 8), (4, 4)])
+@pytest.mark.parametrize("v", [2, 4, 8])
+@pytest.mark.parametrize("k", [64, 100, 256])
+def test_sddmm_random_vs_oracle(pair, v, k):
+    lb, rb = pair
+    s = O.build_sddmm_case(128, 256, k, v, 0.7, lb, rb, seed=k + v)
+    pat = mc.BcrsMatrix(128, 256, v, s["offsets"], s["col_indices"],
+                        mc.PackedArray.from_values(np.ones(s["col_indices"].size * v), 8))
+    out = mc.sddmm(mc.SddmmProblem(mc.pack_dense(s["a"], lb, ROW_MAJOR),
+                                   mc.pack_dense(s["b"], rb, COL_MAJOR), pat))
+    want = O.sddmm(s["a"], s["b"], s["offsets"], s["col_indices"], v, lb, rb)
+    assert (np.asarray(out.values) == want).all()
+
+
+def test_spmm_overflow_raises_like_reference():
+    # L16-R16, K=64, all values 32767: result 64*32767^2 > 2^31 -> OverflowRiskError
+    d = np.full((8, 64), 32767, dtype=np.int64)
+    lhs = mc.bcrs_to_srbcrs(mc.dense_to_bcrs(d, 8, bit_width=16), 16)
+    rhs = mc.pack_dense(np.full((64, 64), 32767), 16)
+    with pytest.raises(mc.OverflowRiskError):
+        mc.spmm(mc.SpmmProblem(lhs, rhs))
+    # the status word is reset: a good problem afterwards succeeds
+    small = mc.pack_dense(np.ones((64, 64), dtype=np.int64), 16)
+    lhs1 = mc.bcrs_to_srbcrs(mc.dense_to_bcrs(np.ones((8, 64), dtype=np.int64), 8, bit_width=16), 16)
+    assert (mc.spmm(mc.SpmmProblem(lhs1, small)) == 64).all()
+
+
+def test_sddmm_overflow_raises():
+    pattern = mc.dense_to_bcrs(np.ones((8, 8), dtype=np.int64), 8)
+    a = mc.pack_dense(np.full((8, 64), -32768), 16, ROW_MAJOR)
+    b = mc.pack_dense(np.full((64, 8), -32768), 16, COL_MAJOR)
+    with pytest.raises(mc.OverflowRiskError):
+        mc.sddmm(mc.SddmmProblem(a, b, pattern))
+
+
+def test_c3_full_size_rows_subset():
+    """Config C3 shape (M=K=4096, N=512, 90%) L8-R8 V=8: check 24 rows against the oracle."""
+    c = O.build_spmm_case(4096, 512, 4096, 8, 0.9, 8, 8, seed=3)
+    lhs = mc.SrBcrsMatrix(4096, 4096, 8, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                          mc.PackedArray.from_values(c["values"], 8))
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], 8)))
+    rows = list(range(0, 512, 23))
+    want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], 8, c["stride"], False,
+                  8, c["rhs"], 8, 4096, rows=rows)
+    got = np.concatenate([out[r * 8:(r + 1) * 8] for r in rows])
+    assert (got == want).all()
