@@ -1,0 +1,404 @@
+"""Benchmark for the Magicube B200 hot path (driver contract: one JSON line on rank 0).
+
+Headline workload (BASELINE.json configs[1], "C2"): SDDMM L8-R8, V=8,
+M=N=4096, K=256 over the sparsity sweep 50/70/90/95/98%. One step = one
+SDDMM launch per sparsity (5 launches) on inputs resident in HBM; the L2 is
+flushed (256 MiB write) before every timed step because the C2 inputs fit in
+L2. metric = TOPS = sum(2*V*K*nblk) / device time. Multi-GPU: one process per
+GPU, each rank runs its own C2 sweep (independent problems, weak scaling, no
+collective in the timed region); time = max over ranks.
+
+`e2e` times the same sweep through the C-ABI entry point mc_sddmm with pinned
+host buffers: every step copies A, B^T and the patterns host->device and the
+int32 block values device->host inside the timed region.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+oracle port, oracle/magicube_ref.py -- the reference itself is pure Python and
+cannot travel to the GPU box) on the same workload and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SPARSITIES = (0.5, 0.7, 0.9, 0.95, 0.98)
+M = N = 4096
+K = 256
+V = 8
+BITS = 8
+FLUSH_BYTES = 256 << 20
+METRIC = "SpMM/SDDMM TOPS vs sparsity & precision pair; sparse-attn seq/s at 1/2/4/8 B200"
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def build_c2(seed_base: int):
+    """C2 inputs with the reference generators (bench.py:113-126 semantics)."""
+    import oracle as O
+    cases = []
+    for s in SPARSITIES:
+        seed = O.cell_seed(seed_base, ((M, N, K), V, s, "L8-R8"))
+        cases.append((s, O.build_sddmm_case(M, N, K, V, s, BITS, BITS, seed)))
+    return cases
+
+
+def sddmm_bytes(nblk: int) -> int:
+    """Algorithmic (compulsory) HBM bytes of one SDDMM launch."""
+    return M * K * BITS // 8 + K * N * BITS // 8 + 4 * nblk + 8 * (M // V + 1) + 4 * V * nblk
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks + throttle reasons while the GPU works."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append(mhz)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv is not None:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def load_traffic(kernel_key: str):
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get(kernel_key)
+    return None
+
+
+def cpu_sweep(cases, rows=None):
+    """The reference algorithm on the host (oracle port): one C2 sweep; returns ops."""
+    import oracle as O
+    ops = 0
+    for s, c in cases:
+        O.sddmm(c["a"], c["b"], c["offsets"], c["col_indices"], V, BITS, BITS)
+        ops += 2 * V * K * int(c["offsets"][-1])
+    return ops
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return
+    cases = build_c2(0)
+    for _ in range(args.warmup):
+        cpu_sweep(cases)
+    times, ops = [], 0
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ops = cpu_sweep(cases)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = ops * args.steps / total / 1e12
+    cores = blas_threads()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TOPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": "C2 SDDMM L8-R8 V=8 M=N=4096 K=256 sparsity 50/70/90/95/98%",
+                   "global_batch": 1, "parallelism": "host"},
+        "cpu_baseline": {"value": value, "unit": "TOPS", "cores": cores, "kind": "port",
+                         "sample": "full C2 sweep per step (oracle/magicube_ref.sddmm, float64 BLAS "
+                                   "gathers, reference int32 semantics)"},
+        "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2209_06979_b200 as mc
+    from paper_2209_06979_b200 import _device as D
+    from paper_2209_06979_b200 import _native as Nn
+
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    lib = Nn.lib()
+    stream = torch.cuda.current_stream()
+    sp = Nn.stream_ptr(stream)
+
+    cases = build_c2(rank)  # weak scaling: every rank owns one independent C2 sweep
+    probs = []
+    for s, c in cases:
+        pat = mc.BcrsMatrix(M, N, V, c["offsets"], c["col_indices"],
+                            mc.PackedArray.from_values(np.ones(c["col_indices"].size * V), 8))
+        a = mc.pack_dense(c["a"], BITS, mc.qint.ROW_MAJOR)
+        b = mc.pack_dense(c["b"], BITS, mc.qint.COL_MAJOR)
+        p = mc.SddmmProblem(a, b, pat)
+        astruct, ka = D.dense_struct(p.a)
+        bstruct, kb = D.dense_struct(p.b)
+        pstruct, kp = D.bcrs_struct(p.out_pattern)
+        nblk = pat.n_blocks
+        out = torch.empty(nblk * V, dtype=torch.int32, device=dev)
+        probs.append(dict(s=s, p=p, a=astruct, b=bstruct, pat=pstruct, keep=(ka, kb, kp), out=out,
+                          nblk=nblk, ops=2 * V * K * nblk, bytes=sddmm_bytes(nblk), c=c))
+    status = D.status_word()
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    def launch(pr):
+        Nn.check(lib.mc_sddmm(pr["a"], pr["b"], pr["pat"], Nn.ptr(pr["out"]), Nn.ptr(status), sp))
+
+    # correctness gate before timing: bit-exact vs the oracle on sampled rows
+    for pr in probs:
+        launch(pr)
+    D.fetch_status(status)
+    import oracle as O
+    for pr in probs:
+        c = pr["c"]
+        rows = range(0, M // V, 61)
+        offs = c["offsets"]
+        for r in rows:
+            lo, hi = int(offs[r]), int(offs[r + 1])
+            want = O.sddmm(c["a"][r * V:(r + 1) * V], c["b"], np.array([0, hi - lo]),
+                           c["col_indices"][lo:hi], V, BITS, BITS)
+            got = pr["out"][lo * V:hi * V].cpu().numpy()
+            assert (got == want).all(), f"SDDMM mismatch at sparsity {pr['s']} row {r}"
+
+    peak_hbm, _, peak_kind = measured_peaks()
+    n_launch = len(probs)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_launch + 1)] for _ in range(args.steps)]
+
+    def step(events=None):
+        if events:
+            events[0].record(stream)
+        for i, pr in enumerate(probs):
+            launch(pr)
+            if events:
+                events[i + 1].record(stream)
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    lib.mc_launch_count(1)
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            lib.mc_l2_flush(Nn.ptr(flush), FLUSH_BYTES, sp)
+            step(ev[i])
+        torch.cuda.synchronize()
+    launches = int(lib.mc_launch_count(0))
+    if world > 1:
+        dist.barrier()
+    per_launch = np.array([[ev[i][j].elapsed_time(ev[i][j + 1]) for j in range(n_launch)]
+                           for i in range(args.steps)])  # ms
+    step_ms = per_launch.sum(axis=1)
+    my_total_ms = float(step_ms.sum())
+    total_ms = my_total_ms
+    if world > 1:
+        t = torch.tensor([my_total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ops_step = sum(pr["ops"] for pr in probs)
+    value = ops_step * world * args.steps / (total_ms * 1e-3) / 1e12
+
+    # roofline of the dominant kernel (the 50% launch, largest bytes)
+    dom = int(np.argmax([pr["bytes"] for pr in probs]))
+    dom_ms = float(per_launch[:, dom].mean())
+    achieved = probs[dom]["bytes"] / (dom_ms * 1e-3) / 1e9
+    sweep = {f"{pr['s']:.2f}": {
+        "tops": pr["ops"] / (float(per_launch[:, j].mean()) * 1e-3) / 1e12,
+        "us": 1e3 * float(per_launch[:, j].mean()),
+        "hbm_gbs": pr["bytes"] / (float(per_launch[:, j].mean()) * 1e-3) / 1e9,
+        "roofline_frac": (pr["bytes"] / (float(per_launch[:, j].mean()) * 1e-3) / 1e9) / peak_hbm,
+    } for j, pr in enumerate(probs)}
+
+    # end-to-end through the C ABI with pinned host buffers
+    e2e = run_e2e(args, probs, lib, Nn, torch, dev, stream, flush, world)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": "C2 SDDMM L8-R8 V=8 M=N=4096 K=256 sparsity 50/70/90/95/98%",
+                   "global_batch": world, "launches_per_step": n_launch,
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"independent C2 sweep per rank x{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
+                     "frac": achieved / peak_hbm, "traffic": load_traffic("sddmm_c2_s0.50"),
+                     "kernel": "sddmm_kernel<8,8,8> @ sparsity 0.50",
+                     "algorithmic_bytes": probs[dom]["bytes"], "peak_kind": peak_kind},
+        "sweep": sweep,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(probs)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, probs, lib, Nn, torch, dev, stream, flush, world):
+    """Same sweep through mc_sddmm with host<->device copies inside the timed region."""
+    from paper_2209_06979_b200 import _device as D
+    host, devb, structs = [], [], []
+    h2d = d2h = 0
+    for pr in probs:
+        c = pr["c"]
+        a_w = torch.from_numpy(pr["p"].a.words.view(np.int32)).pin_memory()
+        b_w = torch.from_numpy(pr["p"].b.words.view(np.int32)).pin_memory()
+        offs = torch.from_numpy(np.asarray(c["offsets"], dtype=np.int64)).pin_memory()
+        cols = torch.from_numpy(np.asarray(c["col_indices"], dtype=np.uint32).view(np.int32)).pin_memory()
+        out_h = torch.empty(pr["nblk"] * V, dtype=torch.int32).pin_memory()
+        d = [torch.empty_like(x, device=dev) for x in (a_w, b_w, offs, cols)]
+        out_d = torch.empty(pr["nblk"] * V, dtype=torch.int32, device=dev)
+        a = Nn.McDense(M, K, BITS, Nn.MC_ROW_MAJOR, Nn.ptr(d[0]))
+        b = Nn.McDense(K, N, BITS, Nn.MC_COL_MAJOR, Nn.ptr(d[1]))
+        pat = Nn.McBcrs(M, N, V, 0, pr["nblk"], Nn.ptr(d[2]), Nn.ptr(d[3]))
+        host.append((a_w, b_w, offs, cols, out_h))
+        devb.append((d, out_d))
+        structs.append((a, b, pat))
+        h2d += sum(x.numel() * x.element_size() for x in (a_w, b_w, offs, cols))
+        d2h += out_h.numel() * 4
+    status = D.status_word()
+    sp = Nn.stream_ptr(stream)
+
+    def step():
+        for (hs, (d, out_d), (a, b, pat)) in zip(host, devb, structs):
+            for src, dst in zip(hs[:4], d):
+                dst.copy_(src, non_blocking=True)
+            Nn.check(lib.mc_sddmm(a, b, pat, Nn.ptr(out_d), Nn.ptr(status), sp))
+            hs[4].copy_(out_d, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.steps):
+        step()
+    s1.record(stream)
+    torch.cuda.synchronize()
+    ms = s0.elapsed_time(s1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # results copied back must equal the device-resident run
+    for (hs, (d, out_d), _), pr in zip(zip(host, devb, structs), probs):
+        assert torch.equal(hs[4], pr["out"].cpu())
+    ops = sum(pr["ops"] for pr in probs)
+    return {"value": ops * world * args.steps / (ms * 1e-3) / 1e12, "unit": "TOPS",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": ms / args.steps, "path": "mc_sddmm (C ABI), pinned host buffers"}
+
+
+def cpu_baseline(probs):
+    """Oracle port on the host cores over a bounded sample (~10-30 s of CPU work)."""
+    cases = [(pr["s"], pr["c"]) for pr in probs]
+    t0 = time.perf_counter()
+    reps = 0
+    ops = 0
+    while time.perf_counter() - t0 < 10.0 and reps < 20:
+        ops += cpu_sweep(cases)
+        reps += 1
+    dt = time.perf_counter() - t0
+    return {"value": ops / dt / 1e12, "unit": "TOPS", "cores": blas_threads(), "kind": "port",
+            "sample": f"{reps} full C2 sweeps (oracle/magicube_ref.sddmm, float64 BLAS gathers) "
+                      f"in {dt:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -178,7 +178,7 @@ sddmm_kernel(const SddmmParams p) {
 
 template <int LB, int RB, int V>
 cudaError_t launch_v(const SddmmParams& p, cudaStream_t s) {
-  const bool aligned = ((p.K * LB / 8) % 16 == 0) && ((p.K * RB / 8) % 16 == 0) &&
+  const bool aligned = ((p.K * LB) % 128 == 0) && ((p.K * RB) % 128 == 0) &&
                        ((reinterpret_cast<uintptr_t>(p.a_words) & 15) == 0) &&
                        ((reinterpret_cast<uintptr_t>(p.b_words) & 15) == 0) &&
                        ((p.a_stride * 4) % 16 == 0) && ((p.b_stride * 4) % 16 == 0);

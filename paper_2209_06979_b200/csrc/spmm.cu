@@ -374,7 +374,7 @@ template <int LB, int RB, int V>
 cudaError_t launch_spmm_v(const SpmmParams& p, cudaStream_t stream) {
   using C = SpmmCfg<LB, RB, V>;
   const int smem = kWarps * kStages * C::STAGE;
-  const bool aligned = ((p.N * RB / 8) % 16 == 0) && ((reinterpret_cast<uintptr_t>(p.rhs_words) & 15) == 0) &&
+  const bool aligned = ((p.N * RB) % 128 == 0) && ((reinterpret_cast<uintptr_t>(p.rhs_words) & 15) == 0) &&
                        ((p.rhs_stride * 4) % 16 == 0);
   const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
   if (grid == 0) return cudaSuccess;
