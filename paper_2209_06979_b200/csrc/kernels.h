@@ -49,8 +49,25 @@ struct SddmmParams {
   int64_t tasks;
 };
 
+struct SddmmTcParams {
+  int64_t M, N, K, vrows, n_blocks;
+  int V;
+  const int64_t* row_offsets;
+  const uint32_t* col_indices;
+  int32_t* out;
+  const double* alpha;
+  double alpha_host;
+  uint16_t* out_f16;
+  int n_panels, n_ctiles;
+  int64_t tiles;
+  int debug;
+};
+
 cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream);
 cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream);
+// dense-tile tcgen05 path (sddmm_tc.cu); launch_sddmm dispatches to it by density
+bool sddmm_tc_supported(const SddmmParams& p);
+cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream);
 
 // SR-BCRS packer (sparse_format.py:284-315)
 cudaError_t launch_srbcrs_plan(const int64_t* row_offsets, int64_t vrows, int stride,

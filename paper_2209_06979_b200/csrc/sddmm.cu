@@ -119,27 +119,34 @@ sddmm_kernel(const SddmmParams p) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[c][j][e] = 0;
 
-    for (int64_t ks = 0; ks < p.K; ks += 64) {
-      const int64_t k0 = ks + 16 * t;
-      uint32_t wa[2][4], wl[2][4], wh[2][4];
-      load_k16<LB, ALIGNED>(A, arow, p.K, k0, a_ok, wa);
-      load_k16<RB, ALIGNED>(Bt, c_lo, p.K, k0, lo_ok, wl);
-      load_k16<RB, ALIGNED>(Bt, c_hi, p.K, k0, hi_ok, wh);
+    // K in chunks of 256: all loads of a chunk are issued before its MMAs (memory-level parallelism)
+    for (int64_t kc = 0; kc < p.K; kc += 256) {
+      uint32_t wa[4][2][4], wl[4][2][4], wh[4][2][4];
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
+      for (int s = 0; s < 4; ++s) {
+        const int64_t k0 = kc + 64 * s + 16 * t;
+        load_k16<LB, ALIGNED>(A, arow, p.K, k0, a_ok, wa[s]);
+        load_k16<RB, ALIGNED>(Bt, c_lo, p.K, k0, lo_ok, wl[s]);
+        load_k16<RB, ALIGNED>(Bt, c_hi, p.K, k0, hi_ok, wh[s]);
+      }
 #pragma unroll
-        for (int j = 0; j < RC; ++j) {
+      for (int s = 0; s < 4; ++s) {
 #pragma unroll
-          for (int c = 0; c < LC; ++c) {
-            const uint32_t a0 = wl[j][2 * half], a2 = wl[j][2 * half + 1];
-            const uint32_t a1 = wh[j][2 * half], a3 = wh[j][2 * half + 1];
-            const uint32_t b0 = wa[c][2 * half], b1 = wa[c][2 * half + 1];
-            const bool au = (RB == 16) && (j == 0);
-            const bool bu = (LB == 16) && (c == 0);
-            if (au && bu) mma16832<true, true>(acc[c][j], a0, a1, a2, a3, b0, b1);
-            else if (au) mma16832<true, false>(acc[c][j], a0, a1, a2, a3, b0, b1);
-            else if (bu) mma16832<false, true>(acc[c][j], a0, a1, a2, a3, b0, b1);
-            else mma16832<false, false>(acc[c][j], a0, a1, a2, a3, b0, b1);
+        for (int half = 0; half < 2; ++half) {
+#pragma unroll
+          for (int j = 0; j < RC; ++j) {
+#pragma unroll
+            for (int c = 0; c < LC; ++c) {
+              const uint32_t a0 = wl[s][j][2 * half], a2 = wl[s][j][2 * half + 1];
+              const uint32_t a1 = wh[s][j][2 * half], a3 = wh[s][j][2 * half + 1];
+              const uint32_t b0 = wa[s][c][2 * half], b1 = wa[s][c][2 * half + 1];
+              const bool au = (RB == 16) && (j == 0);
+              const bool bu = (LB == 16) && (c == 0);
+              if (au && bu) mma16832<true, true>(acc[c][j], a0, a1, a2, a3, b0, b1);
+              else if (au) mma16832<true, false>(acc[c][j], a0, a1, a2, a3, b0, b1);
+              else if (bu) mma16832<false, true>(acc[c][j], a0, a1, a2, a3, b0, b1);
+              else mma16832<false, false>(acc[c][j], a0, a1, a2, a3, b0, b1);
+            }
           }
         }
       }
@@ -201,11 +208,25 @@ cudaError_t launch_lr(const SddmmParams& p, cudaStream_t s) {
 
 }  // namespace
 
+// Path selection: the dense tcgen05 tile kernel reads 3*M*N*K/512 operand bytes through
+// shared memory regardless of the pattern, the gather kernel reads n_blocks*K*bits/8;
+// the crossover on B200 sits near a block density of 8%.
+static int sddmm_path_override() {
+  const char* e = getenv("MCUBE_SDDMM_PATH");
+  if (!e) return 0;
+  if (e[0] == 'd') return 1;  // dense
+  if (e[0] == 'g') return 2;  // gather
+  return 0;
+}
+
 cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream) {
-  // warps per vector row: about 4 groups of 16 blocks each
+  const int ov = sddmm_path_override();
+  const double density = (p.M > 0 && p.N > 0) ? static_cast<double>(p.n_blocks) * p.V / (static_cast<double>(p.M) * p.N) : 0.0;
+  if (ov != 2 && sddmm_tc_supported(p) && (ov == 1 || density >= 0.08)) return launch_sddmm_tc(p, stream);
+  // warps per vector row: about one group of 16 blocks each
   const double avg_groups = p.vrows ? (static_cast<double>(p.n_blocks) / p.vrows) / 16.0 : 0.0;
-  int splits = static_cast<int>(avg_groups / 4.0);
-  p.splits = splits < 1 ? 1 : (splits > 64 ? 64 : splits);
+  int splits = static_cast<int>(avg_groups + 0.999);
+  p.splits = splits < 1 ? 1 : (splits > 256 ? 256 : splits);
   p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.splits;
   switch (p.LB * 100 + p.RB) {
     case 1616: return launch_lr<16, 16>(p, stream);

@@ -233,3 +233,36 @@ def test_c3_full_size_rows_subset():
                   8, c["rhs"], 8, 4096, rows=rows)
     got = np.concatenate([out[r * 8:(r + 1) * 8] for r in rows])
     assert (got == want).all()
+
+
+# ---------------- dense tcgen05 SDDMM path vs gather path ----------------
+
+@pytest.mark.parametrize("path", ["dense", "gather"])
+@pytest.mark.parametrize("v", [2, 4, 8])
+@pytest.mark.parametrize("shape", [(512, 512, 256, 0.5), (1024, 640, 128, 0.9), (264, 300, 256, 0.7),
+                                   (256, 128, 256, 0.98)])
+def test_sddmm_paths_vs_oracle(path, v, shape, monkeypatch):
+    m, n, k, sp = shape
+    monkeypatch.setenv("MCUBE_SDDMM_PATH", path)
+    s = O.build_sddmm_case(m, n, k, v, sp, 8, 8, seed=m + n + v)
+    pat = mc.BcrsMatrix(m, n, v, s["offsets"], s["col_indices"],
+                        mc.PackedArray.from_values(np.ones(s["col_indices"].size * v), 8))
+    out = mc.sddmm(mc.SddmmProblem(mc.pack_dense(s["a"], 8, ROW_MAJOR), mc.pack_dense(s["b"], 8, COL_MAJOR), pat))
+    want = O.sddmm(s["a"], s["b"], s["offsets"], s["col_indices"], v, 8, 8)
+    assert (np.asarray(out.values) == want).all()
+
+
+def test_sddmm_dense_c2_full_size(monkeypatch):
+    """C2 at 50% through the tcgen05 path, checked on sampled rows against the oracle."""
+    monkeypatch.setenv("MCUBE_SDDMM_PATH", "dense")
+    s = O.build_sddmm_case(4096, 4096, 256, 8, 0.5, 8, 8, seed=5)
+    pat = mc.BcrsMatrix(4096, 4096, 8, s["offsets"], s["col_indices"],
+                        mc.PackedArray.from_values(np.ones(s["col_indices"].size * 8), 8))
+    out = np.asarray(mc.sddmm(mc.SddmmProblem(mc.pack_dense(s["a"], 8, ROW_MAJOR),
+                                              mc.pack_dense(s["b"], 8, COL_MAJOR), pat)).values)
+    offs = s["offsets"]
+    for r in list(range(0, 512, 37)) + [511]:
+        lo, hi = int(offs[r]), int(offs[r + 1])
+        want = O.sddmm(s["a"][r * 8:(r + 1) * 8], s["b"], np.array([0, hi - lo]), s["col_indices"][lo:hi],
+                       8, 8, 8)
+        assert (out[lo * 8:hi * 8] == want).all(), r
