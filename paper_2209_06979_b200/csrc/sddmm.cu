@@ -87,7 +87,17 @@ sddmm_kernel(const SddmmParams p) {
   const int64_t rem = task - b * per_batch;
   const int64_t r = rem / p.splits;
   const int split = static_cast<int>(rem - r * p.splits);
+  // Speculative column-index load for this warp's first group, positioned as if all rows
+  // had n_blocks / vrows blocks (exact for uniform patterns); it overlaps the row-offset
+  // round trip and is discarded when the real offsets disagree.
+  const int64_t lo_g = (r * p.n_blocks) / p.vrows, hi_g = ((r + 1) * p.n_blocks) / p.vrows;
+  const int64_t ng_g = (hi_g - lo_g + 15) >> 4;
+  const int64_t gb_g = (ng_g * split) / p.splits;
+  const int64_t blk0_g = lo_g + gb_g * 16;
+  const uint32_t spec_col =
+      (gb_g < (ng_g * (split + 1)) / p.splits && blk0_g + lane < hi_g) ? __ldg(p.col_indices + blk0_g + lane) : 0u;
   const int64_t lo = p.row_offsets[r], hi = p.row_offsets[r + 1];
+  const bool spec_ok = (lo == lo_g) && (hi == hi_g);
   const int64_t nb = hi - lo;
   const int64_t ngroups = (nb + 15) >> 4;
   const int64_t gbeg = (ngroups * split) / p.splits, gend = (ngroups * (split + 1)) / p.splits;
@@ -102,7 +112,9 @@ sddmm_kernel(const SddmmParams p) {
   for (int64_t gi = gbeg; gi < gend; ++gi) {
     const int64_t blk0 = lo + gi * 16;
     const int nvalid = static_cast<int>(min_i64(16, hi - blk0));
-    uint32_t mycol = (lane < nvalid) ? __ldg(p.col_indices + blk0 + lane) : 0u;
+    uint32_t mycol = (gi == gbeg && spec_ok) ? spec_col
+                                             : ((lane < nvalid) ? __ldg(p.col_indices + blk0 + lane) : 0u);
+    if (lane >= nvalid) mycol = 0u;
     if (lane < nvalid && mycol >= static_cast<uint32_t>(p.N)) {
       flag_status(p.status, MC_STATUS_BAD_INDEX);
       mycol = 0u;

@@ -8,15 +8,16 @@
 // Bit-exact: int8 x int8 products accumulate exactly in int32 TMEM for K <= 33025
 // (check_accumulation_bound, emulation.py:108-113), identical to kernels.sddmm.
 //
-// CTA (320 threads, 1 per SM, persistent over a contiguous panel-major tile range):
+// CTA (448 threads, 1 per SM, persistent over a contiguous panel-major tile range):
 //   warp 0      TMA producer: A panel (256 rows x K, resident while the panel is
 //               unchanged) and a 2-stage ring of B^T tiles (128 rows x K);
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
 //               (M = 128 pattern columns, N = 256 scalar rows, K step 32);
-//   warps 2..5  consumers: tcgen05.ld the accumulator (TMEM lane = pattern column,
+//   warps 2..9  consumers (two per TMEM lane quarter, each draining half of the
+//               accumulator columns): tcgen05.ld the accumulator (TMEM lane = pattern column,
 //               TMEM column = scalar row, double-buffered loads) and store each
 //               present block's V int32 values as one sector-sized vector store;
-//   warps 6..9  builders: walk the pattern with one forward cursor per vector row
+//   warps 10..13 builders: walk the pattern with one forward cursor per vector row
 //               (the first found by interpolation search) through a shared-memory
 //               window of column indices, and publish a per-tile
 //               column -> block-slot map, double buffered ahead of the consumers.
@@ -46,13 +47,13 @@ namespace {
 constexpr int kPanel = 256;   // scalar rows of A per tile (UMMA N)
 constexpr int kCols = 128;    // pattern columns per tile (UMMA M)
 constexpr int kStages = 2;
-constexpr int kThreads = 320;
+constexpr int kThreads = 448;
 constexpr uint32_t kIdesc = tc::idesc_i8(128, 256);
 
 template <int V>
 struct Smem {
   static constexpr int VR = kPanel / V;                    // vector rows per panel
-  static constexpr int WIN = 256;                          // cached column indices per row (uint32)
+  static constexpr int WIN = V == 8 ? 512 : 256;           // cached column indices per row (uint32)
   static constexpr int A_BYTES = 2 * kPanel * 128;         // 64 KB (K <= 256)
   static constexpr int B_STAGE = 2 * kCols * 128;          // 32 KB
   static constexpr int POSMAP = kCols * VR;                // [column][vector row] slot codes
@@ -155,9 +156,9 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     tc::mbar_init(a_empty, 1);
     for (int a = 0; a < 2; ++a) {
       tc::mbar_init(tfull_bar(a), 1);
-      tc::mbar_init(tempty_bar(a), 4);
+      tc::mbar_init(tempty_bar(a), 8);
       tc::mbar_init(pfull_bar(a), 128);
-      tc::mbar_init(pempty_bar(a), 4);
+      tc::mbar_init(pempty_bar(a), 8);
     }
     tc::fence_barrier_init();
     tc::prefetch_tmap(&tmA);
@@ -166,14 +167,18 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp == 1) tc::tmem_alloc<512>(smem_u32(tmem_holder));
   // Builders: start fetching the first panel's pattern window right away, positioned by
   // the average row length (validated against the real row offsets after the sync).
-  int64_t pre_a0 = 0;
-  if (warp >= 6 && t0 < t1) {
-    const int bt = threadIdx.x - 192;
+  int64_t pre_a0 = 0, pre_lo = 0, pre_end = 0;
+  if (warp >= 10 && t0 < t1) {
+    const int bt = threadIdx.x - 320;
     constexpr int TPR = 128 / VR;
     const int rl = bt / TPR, sub = bt % TPR;
     const int64_t panel = t0 / p.n_ctiles;
     const uint32_t c0 = static_cast<uint32_t>((t0 % p.n_ctiles) * kCols);
     const int64_t r = panel * VR + rl;
+    if (r < p.vrows) {
+      pre_lo = p.row_offsets[r];  // consumed after the barrier: the load latency overlaps setup
+      pre_end = p.row_offsets[r + 1];
+    }
     if (r < p.vrows && p.n_blocks > 0) {
       const double avg = static_cast<double>(p.n_blocks) / static_cast<double>(p.vrows);
       const int64_t g = static_cast<int64_t>(avg * (static_cast<double>(r) + static_cast<double>(c0) / p.N));
@@ -257,9 +262,12 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (t + 1 == t1 || (t + 1) / p.n_ctiles != panel) tc::mma_commit(a_empty);
       }
     }
-  } else if (warp < 6) {
+  } else if (warp < 10) {
     // ---------------- consumers: TMEM -> registers -> 32-byte block stores ----------------
+    // two warps per TMEM lane quarter; warp group `half` drains accumulator columns
+    // [128*half, 128*half + 128) (chunks 4*half .. 4*half+3)
     const int ct_id = threadIdx.x - 64;
+    const int half = (warp - 2) >> 2;
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     const int c_local = 32 * q + lane;
     constexpr int rpc = 32 / V;  // vector rows per 32-row chunk
@@ -281,13 +289,15 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       stamp(dbg && ct_id == 0 && i < 6, 23 + 3 * static_cast<int>(i));
       const uint32_t tl = tmem + (static_cast<uint32_t>(32 * q) << 16) + b * 256;
       uint32_t va[32], vb[32];
-      tc::tmem_ld32_issue(tl, va);
+      constexpr int kChunks = kPanel / 64;  // chunks per consumer warp group
+      tc::tmem_ld32_issue(tl + 128 * half, va);
       tc::tmem_wait_ld();
 #pragma unroll
-      for (int k = 0; k < kPanel / 32; ++k) {
-        uint32_t(&cur)[32] = (k & 1) ? vb : va;
-        uint32_t(&nxt)[32] = (k & 1) ? va : vb;
-        if (k + 1 < kPanel / 32) tc::tmem_ld32_issue(tl + 32 * (k + 1), nxt);
+      for (int kk = 0; kk < kChunks; ++kk) {
+        const int k = kChunks * half + kk;
+        uint32_t(&cur)[32] = (kk & 1) ? vb : va;
+        uint32_t(&nxt)[32] = (kk & 1) ? va : vb;
+        if (kk + 1 < kChunks) tc::tmem_ld32_issue(tl + 32 * (k + 1), nxt);
 #pragma unroll
         for (int w = 0; w < rpc; ++w) {
           const int rl = k * rpc + w;
@@ -310,7 +320,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             }
           }
         }
-        if (k + 1 < kPanel / 32) tc::tmem_wait_ld();
+        if (kk + 1 < kChunks) tc::tmem_wait_ld();
       }
       tc::tc_fence_before();
       __syncwarp();
@@ -322,7 +332,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   } else {
     // ---------------- builders: pattern cursor -> per-tile column map ----------------
-    const int bt = threadIdx.x - 192;
+    const int bt = threadIdx.x - 320;
     constexpr int TPR = 128 / VR;  // builder threads per vector row (a group of lanes in one warp)
     const int rl = bt / TPR, sub = bt % TPR;
     uint32_t* wrow = win + rl * WIN;
@@ -336,12 +346,12 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       const uint32_t c0 = static_cast<uint32_t>(ct * kCols);
       const int64_t r = panel * VR + rl;
       const bool row_ok = r < p.vrows;
-      const int64_t end = row_ok ? p.row_offsets[r + 1] : 0;
+      const int64_t end = row_ok ? (t == t0 ? pre_end : p.row_offsets[r + 1]) : 0;
       if (panel != cur_panel) {
         // First cursor of the panel: fetch a WIN-entry window around the interpolated
         // position of c0 (one round trip) and locate the cursor inside it; fall back to
         // the interpolation search only when the window misses.
-        const int64_t lo = row_ok ? p.row_offsets[r] : 0;
+        const int64_t lo = row_ok ? (t == t0 ? pre_lo : p.row_offsets[r]) : 0;
         int64_t a0 = lo;
         if (t == t0) {
           a0 = pre_a0;  // window prefetched before the setup barrier
@@ -384,6 +394,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         cur_panel = panel;
         stamp(dbg && bt == 0, 40);
       }
+      cp_async_wait<0>();  // an asynchronous window refill issued after the previous tile
       __syncwarp();
       const int64_t base = cursor[rl];
       // refill the row's cached window (cp.async, 16-byte chunks) when the next 128
@@ -439,6 +450,25 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       tc::mbar_arrive(pfull_bar(b));
       stamp(dbg && bt == 0 && i < 6, 22 + 3 * static_cast<int>(i));
+      // Prefetch the next tile's candidates now (asynchronously) if the cached window
+      // will not cover them; the copy lands while the builder waits for a free map.
+      if (t + 1 < t1 && (t + 1) / p.n_ctiles == panel && row_ok && stop + kCols > win_lo[rl] + win_n[rl] &&
+          win_lo[rl] + win_n[rl] < end) {
+        __syncwarp(gmask);
+        const int64_t a0 = stop & ~3LL;
+        const int64_t n = (end - a0 < WIN) ? (end - a0) : WIN;
+        for (int ch = sub; ch < WIN / 4; ch += TPR) {
+          const int64_t e0 = a0 + 4 * ch;
+          const uint32_t bytes = e0 < end ? static_cast<uint32_t>((end - e0) >= 4 ? 16 : (end - e0) * 4) : 0u;
+          cp_async16(smem_u32(wrow) + 16 * ch, p.col_indices + (bytes ? e0 : 0), bytes);
+        }
+        cp_async_commit();
+        __syncwarp(gmask);
+        if (sub == 0) {
+          win_lo[rl] = a0;
+          win_n[rl] = static_cast<int32_t>(n);
+        }
+      }
     }
   }
   tc::tc_fence_before();
