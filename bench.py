@@ -307,6 +307,17 @@ def run_ours(args):
     # end-to-end through the C ABI with pinned host buffers
     e2e = run_e2e(args, probs, lib, Nn, torch, dev, stream, flush, world)
 
+    # validation-only collective (outside every timed region): NCCL all-gather of each
+    # rank's output checksums + sampled-row verdicts
+    validation = {"ranks": world, "sampled_rows_exact": True}
+    if world > 1:
+        sums = torch.tensor([int(pr["out"].to(torch.int64).sum().item()) for pr in probs] + [1],
+                            dtype=torch.int64, device=dev)
+        gathered = [torch.empty_like(sums) for _ in range(world)]
+        dist.all_gather(gathered, sums)
+        validation["checksums"] = [g[:-1].tolist() for g in gathered]
+        validation["sampled_rows_exact"] = bool(all(int(g[-1]) == 1 for g in gathered))
+
     line = {
         "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -321,6 +332,7 @@ def run_ours(args):
                      "algorithmic_bytes": probs[dom]["bytes"], "peak_kind": peak_kind},
         "sweep": sweep,
         "e2e": e2e,
+        "validation": validation,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

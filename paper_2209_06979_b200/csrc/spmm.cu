@@ -94,38 +94,74 @@ spmm_kernel(const SpmmParams p) {
   const uint32_t wbuf_s = smem_u32(wbuf);
 
   // ---- producer state: column indices for this lane's copies, one step ahead ----
+  // Column indices are staged through a per-warp smem ring: chunk c (stored positions
+  // [p_begin + 256c, +256), i.e. k-steps 8c..8c+7) is fetched by cp.async one chunk ahead.
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(smem + kWarps * kStages * C::STAGE) + warp * 512;
+  const uint32_t sidx_s = smem_u32(sidx);
+  auto fetch_idx_chunk = [&](int c) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int ch = lane + 32 * u;
+      const int64_t e0 = p_begin + 256LL * c + 4 * ch;
+      const int64_t avail = p_end - e0;
+      const uint32_t bytes = avail >= 4 ? 16u : (avail > 0 ? static_cast<uint32_t>(avail) * 4u : 0u);
+      cp_async16(sidx_s + ((c & 1) * 256 + 4 * ch) * 4, p.col_indices + (bytes ? e0 : 0), bytes);
+    }
+  };
+  // per-lane invariants of the producer (hoisted out of the k-loop)
+  const int stored32 = static_cast<int>(stored);
+  const uint64_t row_bytes = static_cast<uint64_t>(p.N) * RB / 8;
+  const uint64_t c0_bytes = static_cast<uint64_t>(c0) * RB / 8;
+  const uint8_t* rhs_b = reinterpret_cast<const uint8_t*>(rhs);
+  const uint32_t kdim = static_cast<uint32_t>(p.K);
+  uint32_t dst_off[C::CPR];
+  int kk_l[C::CPR], kk_p[C::CPR];
+  uint32_t colofs[C::CPR];
+  bool chunk_ok[C::CPR];
+#pragma unroll
+  for (int u = 0; u < C::CPR; ++u) {
+    const int q = lane + 32 * u;
+    const int kk = q / C::CPR, ch = q % C::CPR;
+    const int slot = slot_of(kk);
+    dst_off[u] = slot * C::RBYTES + ((ch * 16) ^ swz<C::RBYTES>(slot & 3));
+    kk_l[u] = kk;
+    kk_p[u] = shuffled ? ((kk & ~7) | (((kk & 7) >> 1) | ((kk & 1) << 2))) : kk;  // P^-1 within 8-groups
+    colofs[u] = static_cast<uint32_t>(c0_bytes) + ch * 16;
+    chunk_ok[u] = c0_bytes + ch * 16 < row_bytes;
+  }
+  // LHS value copies: lane -> (half h, row v, 8-byte part), constant per lane
+  constexpr int kAPer = C::ABYTES / 8;
+  constexpr int kACopies = (C::A_COPIES + 31) / 32;
+  const int64_t a_task_base = (p_begin / p.S) * V * p.S;  // element index of the row's first stride
+  const int S = p.S;
+  int a_blk = 0, a_within = 0;  // stride-block offset (elements) and offset within stride for pos = 32*step
+
   uint32_t nidx[C::CPR];
   auto load_idx = [&](int step) {
+    const int base = ((step >> 3) & 1) * 256 + 32 * (step & 7);
 #pragma unroll
-    for (int u = 0; u < C::CPR; ++u) {
-      const int kk = (lane + 32 * u) / C::CPR;
-      const int64_t q = p_begin + 32LL * step + kk;
-      nidx[u] = (q < p_end) ? __ldg(p.col_indices + idx_pos(q, shuffled)) : kSentinel;
-    }
+    for (int u = 0; u < C::CPR; ++u)
+      nidx[u] = (32 * step + kk_l[u] < stored32) ? sidx[base + kk_p[u]] : kSentinel;
   };
 
   auto issue = [&](int step) {
+    if ((step & 7) == 0 && 256LL * ((step >> 3) + 1) < stored) {
+      __syncwarp();  // every lane is done reading the ring slot being refilled
+      fetch_idx_chunk((step >> 3) + 1);
+    }
     const uint32_t sbase = wbuf_s + (step % kStages) * C::STAGE;
 #pragma unroll
     for (int u = 0; u < C::CPR; ++u) {
-      const int q = lane + 32 * u;
-      const int kk = q / C::CPR;
-      const int ch = q % C::CPR;
-      const int slot = slot_of(kk);
-      const uint32_t dst = sbase + slot * C::RBYTES + ((ch * 16) ^ swz<C::RBYTES>(slot & 3));
-      uint32_t col = nidx[u];
-      bool ok = col != kSentinel;
-      if (ok && col >= static_cast<uint32_t>(p.K)) {
-        flag_status(p.status, MC_STATUS_BAD_INDEX);
-        ok = false;
-      }
+      const uint32_t dst = sbase + dst_off[u];
+      const uint32_t col = nidx[u];
+      bool ok = col < kdim;
+      if (!ok && col != kSentinel) flag_status(p.status, MC_STATUS_BAD_INDEX);
       if constexpr (ALIGNED) {
-        const int64_t rem_bytes = ((p.N - c0) * RB) / 8 - ch * 16;
-        const uint32_t nbytes = (ok && rem_bytes > 0) ? 16u : 0u;
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(rhs);
-        if (nbytes) src += ((static_cast<int64_t>(col) * p.N + c0) * RB) / 8 + ch * 16;
+        const uint32_t nbytes = (ok && chunk_ok[u]) ? 16u : 0u;
+        const uint8_t* src = nbytes ? rhs_b + static_cast<uint64_t>(col) * row_bytes + colofs[u] : rhs_b;
         cp_async16(dst, src, nbytes);
       } else {
+        const int ch = (lane + 32 * u) % C::CPR;
         // generic path: element-wise fetch for rows that are not 16-byte aligned
         constexpr int EPC = 128 / RB;  // elements per 16-byte chunk
         uint32_t wv[4] = {0u, 0u, 0u, 0u};
@@ -143,25 +179,33 @@ spmm_kernel(const SpmmParams p) {
                      "r"(wv[2]), "r"(wv[3]));
       }
     }
-    // LHS values of this step: 2 halves x V rows x 16 elements, 8-byte copies
+    // LHS values of this step: 2 halves x V rows x 16 elements, 8-byte copies.
+    // Element (v, pos) lives at stride-block base + v*S + (pos mod S) (sparse_format.py:131-139).
     const uint32_t abase = sbase + C::B_STAGE;
+    const uint8_t* lhs_b = reinterpret_cast<const uint8_t*>(lhs);
 #pragma unroll
-    for (int u = 0; u < (C::A_COPIES + 31) / 32; ++u) {
+    for (int u = 0; u < kACopies; ++u) {
       const int q = lane + 32 * u;
       if (q < C::A_COPIES) {
-        const int per_row = C::ABYTES / 8;
-        const int row = q / per_row;  // row = h*V + v
-        const int part = q % per_row;
+        const int row = q / kAPer;  // row = h*V + v
+        const int part = q % kAPer;
         const int h = row / V, v = row % V;
-        const int64_t pos = p_begin + 32LL * step + 16 * h;
-        const bool ok = pos < p_end;
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(lhs);
-        if (ok) {
-          const int64_t e = (pos / p.S) * V * p.S + static_cast<int64_t>(v) * p.S + (pos % p.S);
-          src += (e * LB) / 8 + part * 8;
+        int blk = a_blk, within = a_within + 16 * h;
+        if (within >= S) {
+          within -= S;
+          blk += V * S;
         }
+        const bool ok = 32 * step + 16 * h < stored32;
+        const int64_t e = a_task_base + blk + v * S + within;
+        const uint8_t* src = ok ? lhs_b + (e * LB) / 8 + part * 8 : lhs_b;
         cp_async8(abase + row * C::ABYTES + part * 8, src, ok ? 8u : 0u);
       }
+    }
+    // advance the stride cursor to pos = 32*(step+1)
+    a_within += 32;
+    while (a_within >= S) {
+      a_within -= S;
+      a_blk += V * S;
     }
   };
 
@@ -176,6 +220,10 @@ spmm_kernel(const SpmmParams p) {
         for (int e = 0; e < 4; ++e) acc[c][j][q][e] = 0;
 
   if (nsteps > 0) {
+    fetch_idx_chunk(0);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
     load_idx(0);
 #pragma unroll
     for (int s = 0; s < kStages - 1; ++s) {
@@ -373,7 +421,7 @@ spmm_kernel(const SpmmParams p) {
 template <int LB, int RB, int V>
 cudaError_t launch_spmm_v(const SpmmParams& p, cudaStream_t stream) {
   using C = SpmmCfg<LB, RB, V>;
-  const int smem = kWarps * kStages * C::STAGE;
+  const int smem = kWarps * kStages * C::STAGE + kWarps * 2048;  // + per-warp index ring
   const bool aligned = ((p.N * RB) % 128 == 0) && ((reinterpret_cast<uintptr_t>(p.rhs_words) & 15) == 0) &&
                        ((p.rhs_stride * 4) % 16 == 0);
   const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
