@@ -16,7 +16,7 @@ from .errors import (FormatError, OverflowRiskError, QsparseError, ShuffleStateE
                      UnsupportedPrecisionError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmcube.so")
+LIB_PATH = os.environ.get("MCUBE_LIB_PATH") or os.path.join(_HERE, "libmcube.so")  # override: debug builds
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "mcube.h")
 
 MC_OK = 0

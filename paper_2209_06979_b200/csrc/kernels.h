@@ -55,9 +55,12 @@ struct SddmmTcParams {
   const int64_t* row_offsets;
   const uint32_t* col_indices;
   int32_t* out;
+  int64_t out_stride;
   const double* alpha;
   double alpha_host;
   uint16_t* out_f16;
+  int64_t f16_stride;
+  uint32_t* status;
   int n_panels, n_ctiles;
   int64_t tiles;
   int debug;

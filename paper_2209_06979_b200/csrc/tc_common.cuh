@@ -23,13 +23,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// Blocking wait on an mbarrier phase. The suspend-time hint lets the hardware park the
+// warp until the phase completes instead of re-polling (polling warps compete with the
+// shared-memory atomics of the pattern builders).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)
       : "memory");
 }
 

@@ -266,3 +266,93 @@ def test_sddmm_dense_c2_full_size(monkeypatch):
         want = O.sddmm(s["a"][r * 8:(r + 1) * 8], s["b"], np.array([0, hi - lo]), s["col_indices"][lo:hi],
                        8, 8, 8)
         assert (out[lo * 8:hi * 8] == want).all(), r
+
+
+def _irregular_pattern(m, n, v, seed):
+    """Rows with skewed column distributions: empty rows, full rows, clustered rows
+    (defeats the interpolation probe of the dense path and exercises its fallback)."""
+    rng = np.random.default_rng(seed)
+    offs, cols = [0], []
+    for r in range(m // v):
+        kind = r % 5
+        if kind == 0:
+            c = np.array([], dtype=np.int64)
+        elif kind == 1:
+            c = np.arange(n)
+        elif kind == 2:  # clustered at the start
+            c = np.arange(min(n, 3 + r % 97))
+        elif kind == 3:  # clustered at the end
+            c = np.arange(max(0, n - 5 - r % 211), n)
+        else:
+            c = np.sort(rng.choice(n, size=int(rng.integers(0, n)), replace=False))
+        cols.append(c.astype(np.uint32))
+        offs.append(offs[-1] + c.size)
+    return np.array(offs, dtype=np.int64), np.concatenate(cols) if cols else np.zeros(0, np.uint32)
+
+
+@pytest.mark.parametrize("v", [2, 4, 8])
+@pytest.mark.parametrize("shape", [(1024, 2048, 256), (768, 1000, 128), (2048, 384, 256)])
+def test_sddmm_dense_irregular_rows(v, shape, monkeypatch):
+    m, n, k = shape
+    monkeypatch.setenv("MCUBE_SDDMM_PATH", "dense")
+    rng = np.random.default_rng(m + n + k + v)
+    offs, cols = _irregular_pattern(m, n, v, m + v)
+    a = rng.integers(-128, 128, size=(m, k))
+    b = rng.integers(-128, 128, size=(k, n))
+    pat = mc.BcrsMatrix(m, n, v, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * v), 8))
+    out = mc.sddmm(mc.SddmmProblem(mc.pack_dense(a, 8, ROW_MAJOR), mc.pack_dense(b, 8, COL_MAJOR), pat))
+    want = O.sddmm(a, b, offs, cols, v, 8, 8)
+    assert (np.asarray(out.values) == want).all()
+
+
+@pytest.mark.parametrize("sparsity", [0.5, 0.7, 0.9, 0.95, 0.98])
+def test_sddmm_dense_c2_all_rows(sparsity, monkeypatch):
+    """Every C2 sparsity through the tcgen05 path, all rows against the oracle."""
+    monkeypatch.setenv("MCUBE_SDDMM_PATH", "dense")
+    s = O.build_sddmm_case(4096, 4096, 256, 8, sparsity, 8, 8, seed=11)
+    pat = mc.BcrsMatrix(4096, 4096, 8, s["offsets"], s["col_indices"],
+                        mc.PackedArray.from_values(np.ones(s["col_indices"].size * 8), 8))
+    out = np.asarray(mc.sddmm(mc.SddmmProblem(mc.pack_dense(s["a"], 8, ROW_MAJOR),
+                                              mc.pack_dense(s["b"], 8, COL_MAJOR), pat)).values)
+    want = O.sddmm(s["a"], s["b"], s["offsets"], s["col_indices"], 8, 8, 8)
+    assert (out == want).all()
+
+
+@pytest.mark.parametrize("v", [4, 8])
+def test_sddmm_dense_batched_with_f16_epilogue(v, monkeypatch):
+    """mc_sddmm_batched on the tcgen05 path: 3 items sharing one pattern, int32 + fp16 outputs."""
+    import torch
+    from paper_2209_06979_b200 import _native as Nn
+    monkeypatch.setenv("MCUBE_SDDMM_PATH", "dense")
+    m, n, k, batch = 640, 896, 128, 3
+    s = O.build_sddmm_case(m, n, k, v, 0.8, 8, 8, seed=21)
+    offs, cols = s["offsets"], s["col_indices"]
+    rng = np.random.default_rng(3)
+    a = rng.integers(-128, 128, size=(batch, m, k)).astype(np.int8)
+    bt = rng.integers(-128, 128, size=(batch, n, k)).astype(np.int8)  # B^T row-major = B col-major
+    dev = torch.device("cuda", 0)
+    a_d = torch.from_numpy(a.reshape(-1).view(np.int32).copy()).to(dev)
+    b_d = torch.from_numpy(bt.reshape(-1).view(np.int32).copy()).to(dev)
+    o_d = torch.from_numpy(offs.astype(np.int64)).to(dev)
+    c_d = torch.from_numpy(cols.astype(np.uint32).view(np.int32)).to(dev)
+    nblk = cols.size
+    out = torch.empty(batch * nblk * v, dtype=torch.int32, device=dev)
+    out16 = torch.empty(batch * nblk * v, dtype=torch.float16, device=dev)
+    alpha = torch.tensor([0.25, 1.0 / 3.0, 1e-3], dtype=torch.float64, device=dev)
+    ad = Nn.McDense(m, k, 8, Nn.MC_ROW_MAJOR, Nn.ptr(a_d))
+    bd = Nn.McDense(k, n, 8, Nn.MC_COL_MAJOR, Nn.ptr(b_d))
+    pd = Nn.McBcrs(m, n, v, 0, nblk, Nn.ptr(o_d), Nn.ptr(c_d))
+    epi = Nn.McEpilogue(Nn.ptr(alpha), 0.0, Nn.ptr(out16), nblk * v)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = Nn.lib()
+    Nn.check(lib.mc_sddmm_batched(ad, m * k // 4, bd, n * k // 4, pd, batch, epi, Nn.ptr(out), nblk * v,
+                                  Nn.ptr(status), Nn.stream_ptr()))
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    got = out.view(batch, -1).cpu().numpy()
+    got16 = out16.view(batch, -1).cpu().numpy()
+    for i in range(batch):
+        want = O.sddmm(a[i].astype(np.int64), bt[i].T.astype(np.int64), offs, cols, v, 8, 8)
+        assert (got[i] == want).all(), i
+        w16 = (want.astype(np.float64) * float(alpha[i])).astype(np.float16)
+        assert (got16[i].view(np.uint16) == w16.view(np.uint16)).all(), i

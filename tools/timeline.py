@@ -10,6 +10,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 os.environ["MCUBE_DEBUG_TIMELINE"] = "1"
+os.environ.setdefault("MCUBE_LIB_PATH", os.path.join(ROOT, "paper_2209_06979_b200", "libmcube_timeline.so"))
 os.environ["MCUBE_SDDMM_PATH"] = "dense"
 
 import oracle as O  # noqa: E402
@@ -33,9 +34,9 @@ for rep in range(3):
     torch.cuda.synchronize()
     print("kernel ms", e0.elapsed_time(e1))
 lib = _native.load()
-buf = (ctypes.c_ulonglong * (148 * 64))()
-lib.mc_debug_timeline(buf, 148 * 64)
-t = np.frombuffer(buf, dtype=np.uint64).reshape(148, 64).astype(np.int64)
+buf = (ctypes.c_ulonglong * (148 * 128))()
+lib.mc_debug_timeline(buf, 148 * 128)
+t = np.frombuffer(buf, dtype=np.uint64).reshape(148, 128).astype(np.int64)
 base = t[:, 0].min()
 names = {0: "start", 1: "setup", 40: "search", 63: "end"}
 for i in range(6):
@@ -45,6 +46,14 @@ for i in range(6):
     names[22 + 3 * i] = f"ep_built{i}"
     names[23 + 3 * i] = f"ep_full{i}"
     names[24 + 3 * i] = f"ep_done{i}"
+for i in range(5):
+    names[41 + 4 * i] = f"p1start{i}"
+    names[42 + 4 * i] = f"p1done{i}"
+    names[43 + 4 * i] = f"pempty_ok{i}"
+for i in range(5):
+    for w in range(4):
+        names[64 + 8 * i + w] = f"p1w{w}_{i}"
+        names[68 + 8 * i + w] = f"p2w{w}_{i}"
 for cta in (0, 1, 77, 147):
     row = t[cta]
     ev = sorted((int(v - base), names.get(k, str(k))) for k, v in enumerate(row) if v >= base and v != 0)
