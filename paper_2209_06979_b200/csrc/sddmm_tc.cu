@@ -11,18 +11,18 @@
 // 32-column tcgen05.ld, the V contiguous values of block (r, c) for 32/V vector rows,
 // so every present block leaves the SM as one V*4-byte vector store.
 //
-// CTA (448 threads, 1 per SM, persistent over a contiguous tile range, panel-major):
+// CTA (576 threads, 1 per SM, persistent over a contiguous tile range, panel-major):
 //   warp 0      TMA producer: A panel (32*V rows x K, resident while the panel is
 //               unchanged) and a 2-stage (V=8) / 3-stage (V=4) ring of B^T tiles;
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; two accumulators
 //               so the MMA of tile i+1 overlaps the drain of tile i;
-//   warps 2..5  pattern builders, 8 vector rows each, 4 lanes per row: one cursor per
+//   warps 2..9  pattern builders, 4 vector rows each, 8 lanes per row: one cursor per
 //               row into its CSR column list (located once per panel segment by an
 //               interpolation probe + binary search), the list streamed through a
 //               per-row shared-memory ring prefetched by position; per tile a 128-bit
 //               column bitmap per vector row plus the CSR position of each 32-column
 //               quarter, into a 4-deep map ring;
-//   warps 6..13 consumers, two per TMEM lane quarter (each drains half of the
+//   warps 10..17 consumers, two per TMEM lane quarter (each drains half of the
 //               accumulator columns): bit test + popcount give the output block position.
 #include <cuda_fp16.h>
 
@@ -55,12 +55,14 @@ namespace {
 
 constexpr int kVRows = 32;    // vector rows per tile: 32*V scalar rows of A (UMMA N)
 constexpr int kCols = 128;   // pattern columns per tile (UMMA M)
-constexpr int kRing = 4;     // pattern-map ring
-constexpr int kBuildWarps = 4;
+constexpr int kRing = 4;     // pattern-map ring (power of two: slot = i & 3, phase = i >> 2)
+constexpr int kBuildWarps = 8;
 constexpr int kConsWarps = 8;
 constexpr int kFirstBuild = 2;
 constexpr int kFirstCons = kFirstBuild + kBuildWarps;
 constexpr int kThreads = 32 * (kFirstCons + kConsWarps);
+constexpr int kRowsPerBuilder = 32 / kBuildWarps;       // vector rows per builder warp
+constexpr int kLanesPerRow = 32 / kRowsPerBuilder;      // builder lanes per vector row
 constexpr int kRingStride = 516;  // uint32 per row ring (512 + 4 pad)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -132,6 +134,30 @@ __device__ int64_t warp_lower_bound(const uint32_t* __restrict__ cols, int64_t l
   return a;
 }
 
+// Tile coordinates advanced incrementally (a 64-bit division per tile costs a software
+// routine on every role's critical path). Tiles are ordered item-major, then panel, then
+// 128-column tile.
+struct TileCursor {
+  long long item, panel, ct, gpanel;
+  int n_panels, n_ctiles;
+  __device__ TileCursor(long long t, int np, int nc) : n_panels(np), n_ctiles(nc) {
+    gpanel = t / nc;
+    ct = t - gpanel * nc;
+    item = gpanel / np;
+    panel = gpanel - item * np;
+  }
+  __device__ __forceinline__ void next() {
+    if (++ct == n_ctiles) {
+      ct = 0;
+      ++gpanel;
+      if (++panel == n_panels) {
+        panel = 0;
+        ++item;
+      }
+    }
+  }
+};
+
 template <int V>
 __global__ void __launch_bounds__(kThreads, 1)
 sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -165,6 +191,64 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   const int64_t t1 = (p.tiles * (blockIdx.x + 1)) / gridDim.x;
   const int64_t tiles_per_item = static_cast<int64_t>(p.n_panels) * p.n_ctiles;
 
+  // ---- pattern-builder state; their first loads are issued before the setup barrier ----
+  const int bw = warp - kFirstBuild;
+  const int jr = lane / kLanesPerRow, sub = lane % kLanesPerRow;
+  const int rl = kRowsPerBuilder * bw + jr;  // builder lane's vector row within the tile
+  uint32_t* rrow = reinterpret_cast<uint32_t*>(smem + L::OFF_RING) + (rl & (VR - 1)) * kRingStride;
+  const uint32_t rrow_s = smem_u32(rrow);
+  // lane (j, s) issues its quarter of chunks [c_from, c_to) of row j; chunk c of a row
+  // starting at `lo` covers absolute positions [((lo >> 6) + c) * 64, +64)
+  auto fetch_chunks = [&](long long lo_, int c_from, int c_to) {
+    for (int c = c_from; c < c_to; ++c) {
+      const long long base = ((lo_ >> 6) + c) * 64;
+#pragma unroll
+      for (int u = 0; u < 16 / kLanesPerRow; ++u) {
+        const long long pos0 = base + (sub * (16 / kLanesPerRow) + u) * 4;
+        const long long avail = p.n_blocks - pos0;
+        const uint32_t bytes = avail >= 4 ? 16u : (avail > 0 ? static_cast<uint32_t>(avail) * 4u : 0u);
+        cp_async16(rrow_s + static_cast<uint32_t>(pos0 & 511) * 4, p.col_indices + (bytes ? pos0 : 0), bytes);
+      }
+    }
+  };
+  // chunks kept in flight past the cursor: two tiles' worth of entries at the row's density
+  auto prefetch_depth = [&](int len_) {
+    const int per_tile = static_cast<int>((static_cast<long long>(len_) * kCols + p.N - 1) / p.N);
+    const int d = (2 * per_tile + 48 + 63) / 64 + 1;
+    return d < 2 ? 2 : (d > 7 ? 7 : d);
+  };
+  // probe window [chunk x, chunk y) around the interpolated position of c0 (<= 8 chunks)
+  auto probe_window = [&](int len_, uint32_t c0_, int lo63_) {
+    int start = 0, end = 0;
+    const int per_tile = static_cast<int>((static_cast<long long>(len_) * kCols + p.N - 1) / p.N);
+    if (c0_ > 0) {
+      const int g = static_cast<int>((static_cast<double>(c0_) / static_cast<double>(p.N)) * len_);
+      const int margin = 64 + len_ / 16;
+      start = g - margin > 0 ? g - margin : 0;
+      end = g + margin;
+    }
+    end += 2 * per_tile + 48;
+    if (end > len_) end = len_;
+    const int cs = (lo63_ + start) >> 6;
+    int ce = ((lo63_ + (end > 0 ? end - 1 : 0)) >> 6) + 1;
+    if (ce > cs + 8) ce = cs + 8;
+    if (ce < cs + 1) ce = cs + 1;
+    return make_int2(cs, ce);
+  };
+  long long lo = 0, b_lo = 0, b_hi = 0, spec_lo = -1, spec_hi = -1;
+  int len = 0, cur = 0, mtop = 0, landed = 0, lo511 = 0, lo63 = 0, depth = 2, c_first = 0;
+  int mtop_last = 0;  // chunk bound of all cp.async groups but the most recent one
+  long long b_r = -1;
+  uint32_t b_c00 = 0;
+  if (warp >= kFirstBuild && warp < kFirstCons && t0 < t1) {
+    const int64_t rem0 = t0 % tiles_per_item;
+    b_r = (rem0 / p.n_ctiles) * VR + rl;
+    b_c00 = static_cast<uint32_t>((rem0 % p.n_ctiles) * kCols);
+    if (b_r < p.vrows) {  // the first panel's row offsets: in flight across the setup barrier
+      b_lo = p.row_offsets[b_r];
+      b_hi = p.row_offsets[b_r + 1];
+    }
+  }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(full_bar(s), 1);
@@ -196,11 +280,10 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (lane == 0) {
       int64_t cur_panel = -1;
       int n_a = 0;
-      for (int64_t t = t0; t < t1; ++t) {
-        const int64_t i = t - t0;
-        const int64_t item = t / tiles_per_item, rem = t % tiles_per_item;
-        const int64_t panel = rem / p.n_ctiles, ct = rem % p.n_ctiles;
-        const int64_t gpanel = t / p.n_ctiles;
+      TileCursor tc_(t0, p.n_panels, p.n_ctiles);
+      for (int64_t t = t0; t < t1; ++t, tc_.next()) {
+        const int i = static_cast<int>(t - t0);
+        const long long item = tc_.item, panel = tc_.panel, ct = tc_.ct, gpanel = tc_.gpanel;
         if (gpanel != cur_panel) {
           if (n_a > 0) tc::mbar_wait(a_empty, (n_a - 1) & 1);
           tc::mbar_arrive_expect_tx(a_full, KB * PANEL * 128);
@@ -225,9 +308,10 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (lane == 0) {
       int64_t cur_panel = -1;
       int n_a = 0;
-      for (int64_t t = t0; t < t1; ++t) {
-        const int64_t i = t - t0;
-        const int64_t gpanel = t / p.n_ctiles;
+      TileCursor tc_(t0, p.n_panels, p.n_ctiles);
+      for (int64_t t = t0; t < t1; ++t, tc_.next()) {
+        const int i = static_cast<int>(t - t0);
+        const long long gpanel = tc_.gpanel;
         if (gpanel != cur_panel) {
           tc::mbar_wait(a_full, n_a & 1);
           ++n_a;
@@ -253,94 +337,77 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         tc::mma_commit(empty_bar(s));
         tc::mma_commit(tfull_bar(acc));
         MC_STAMP(i < 6, 16 + static_cast<int>(i));
-        if (t + 1 == t1 || (t + 1) / p.n_ctiles != gpanel) tc::mma_commit(a_empty);
+        if (t + 1 == t1 || tc_.ct + 1 == p.n_ctiles) tc::mma_commit(a_empty);  // panel's last tile
       }
     }
   } else if (warp < kFirstCons) {
     // ---------------- pattern builders (4 independent warps) ----------------
-    // Builder warp bw owns vector rows 8*bw .. 8*bw+7 of the tile; lane = (row j, sub s),
-    // four lanes per row. Each row streams its CSR column list through a 512-entry ring
-    // in shared memory (eight 64-entry chunks, absolute position x in slot x & 511),
-    // fetched by POSITION with cp.async up to 8 chunks from the cursor's chunk, so the
-    // chunks a tile reads were issued at least one tile earlier. Positions are relative
-    // to the row start (32-bit). A tile takes at most 128 entries of a row (columns are
-    // strictly increasing). Per tile, lane (j, s) tests candidates s, s+4, s+8, ... of
-    // row j, the four lanes OR their bitmaps with two shuffles, and lane (j, s) writes
-    // the QuarterMap of quarter s. No cross-warp synchronisation: each warp arrives on
-    // the tile's pfull barrier when its rows are published.
-    const int bw = warp - kFirstBuild;
-    const int jr = lane >> 2, sub = lane & 3;
-    const int rl = 8 * bw + jr;  // this lane's vector row within the tile
-    uint32_t* rrow = reinterpret_cast<uint32_t*>(smem + L::OFF_RING) + rl * kRingStride;
-    const uint32_t rrow_s = smem_u32(rrow);
-    // lane (j, s) issues its quarter of chunks [c_from, c_to) of row j; chunk c of a row
-    // starting at `lo` covers absolute positions [((lo >> 6) + c) * 64, +64)
-    auto fetch_chunks = [&](long long lo, int c_from, int c_to) {
-      for (int c = c_from; c < c_to; ++c) {
-        const long long base = ((lo >> 6) + c) * 64;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const long long pos0 = base + (sub * 4 + u) * 4;
-          const long long avail = p.n_blocks - pos0;
-          const uint32_t bytes = avail >= 4 ? 16u : (avail > 0 ? static_cast<uint32_t>(avail) * 4u : 0u);
-          cp_async16(rrow_s + static_cast<uint32_t>(pos0 & 511) * 4, p.col_indices + (bytes ? pos0 : 0), bytes);
-        }
-      }
-    };
-    long long lo = 0;
-    int len = 0, cur = 0, mtop = 0, lo511 = 0, lo63 = 0;
-    // first panel's row offsets: issued before anything waits on them
-    long long pre_lo = 0, pre_hi = 0;
-    if (t0 < t1) {
-      const long long r = ((t0 % tiles_per_item) / p.n_ctiles) * VR + rl;
-      if (r < p.vrows) {
-        pre_lo = p.row_offsets[r];
-        pre_hi = p.row_offsets[r + 1];
-      }
+    // Builder warp bw owns vector rows 4*bw .. 4*bw+3 of the tile; lane = (row j, sub s),
+    // eight lanes per row. Each row streams its CSR column list through a 512-entry ring
+    // in shared memory (64-entry chunks, absolute position x in slot x & 511), fetched by
+    // POSITION with cp.async `depth` chunks ahead of the cursor (depth follows the row's
+    // density). Reads are bounded by the chunks known to have landed; a tile that runs
+    // past them waits (cp.async.wait_all). Positions are relative to the row start.
+    // Per tile, lane (j, s) tests candidates s, s+8, s+16, ... of row j until the row
+    // leaves the tile (columns strictly increasing), the eight lanes OR their bitmaps with
+    // three shuffles, and lane (j, s < 4) writes the QuarterMap of quarter s. No cross-warp
+    // synchronisation: each warp arrives on the tile's pfull barrier.
+    if (b_r >= 0 && b_r < p.vrows) {
+      // speculate rows of equal length (exact for the reference generator's patterns):
+      // the window fetch overlaps the offsets round trip and is discarded if wrong
+      spec_lo = (b_r * p.n_blocks) / p.vrows;
+      spec_hi = ((b_r + 1) * p.n_blocks) / p.vrows;
+      const int slen = static_cast<int>(spec_hi - spec_lo);
+      const int2 w = probe_window(slen, b_c00, static_cast<int>(spec_lo & 63));
+      c_first = w.x;
+      if (slen > 0) fetch_chunks(spec_lo, w.x, w.y);
+      mtop = w.y;
     }
+    cp_async_commit();
     int64_t cur_panel = -1;
-    for (int64_t t = t0; t < t1; ++t) {
-      const int64_t i = t - t0;
-      const int slot = static_cast<int>(i % kRing);
-      const int64_t rem = t % tiles_per_item;
-      const int64_t panel = rem / p.n_ctiles, ct = rem % p.n_ctiles;
-      const int64_t gpanel = t / p.n_ctiles;
+    TileCursor tc_(t0, p.n_panels, p.n_ctiles);
+    for (int64_t t = t0; t < t1; ++t, tc_.next()) {
+      const int i = static_cast<int>(t - t0);
+      const int slot = i & (kRing - 1);
+      const long long panel = tc_.panel, ct = tc_.ct, gpanel = tc_.gpanel;
       const uint32_t c0 = static_cast<uint32_t>(ct * kCols);
       if (gpanel != cur_panel) {
         // ---- segment start: locate the row's cursor at column c0 ----
-        cp_async_wait<0>();
-        __syncwarp();
-        long long hi = pre_hi;
-        lo = pre_lo;
-        if (t != t0) {
+        long long hi;
+        bool spec_ok;
+        if (t == t0) {  // offsets + speculative window were issued before the setup barrier
+          lo = b_lo;
+          hi = b_hi;
+          spec_ok = (lo == spec_lo) && (hi == spec_hi);
+        } else {
           const long long r = panel * VR + rl;
           lo = hi = 0;
           if (r < p.vrows) {
             lo = p.row_offsets[r];
             hi = p.row_offsets[r + 1];
           }
+          spec_ok = false;
         }
         len = static_cast<int>(hi - lo);
         lo63 = static_cast<int>(lo & 63);
         lo511 = static_cast<int>(lo & 511);
-        int start = 0;  // probe window start (relative)
-        if (c0 > 0 && len > 512) {  // interpolated position of c0, minus a margin
-          const int g = static_cast<int>((static_cast<double>(c0) / static_cast<double>(p.N)) * len);
-          start = g - 192;
-          if (start > len - 512) start = len - 512;
-          if (start < 0) start = 0;
+        depth = prefetch_depth(len);
+        cp_async_wait<0>();  // nothing of an older window may land after the new copies
+        if (!spec_ok) {
+          const int2 w = probe_window(len, c0, lo63);
+          c_first = w.x;
+          if (len > 0) fetch_chunks(lo, w.x, w.y);
+          mtop = w.y;
+          cp_async_commit();
+          cp_async_wait<0>();
         }
-        const int c_start = (lo63 + start) >> 6;
-        if (len > 0) fetch_chunks(lo, c_start, c_start + 8);
-        cp_async_commit();
-        cp_async_wait<0>();
         __syncwarp();
+        landed = mtop_last = mtop;
         cur = 0;
-        mtop = c_start + 8;
-        if (c0 > 0) {
-          // lower bound of c0 inside the fetched window [ws, we) (binary search in smem)
-          const int ws = (c_start * 64 - lo63 > 0) ? c_start * 64 - lo63 : 0;
-          const int we = ((c_start + 8) * 64 - lo63 < len) ? (c_start + 8) * 64 - lo63 : len;
+        if (c0 > 0 && len > 0) {
+          // lower bound of c0 inside the landed window [ws, we) (binary search in smem)
+          const int ws = (c_first * 64 - lo63 > 0) ? c_first * 64 - lo63 : 0;
+          const int we = (landed * 64 - lo63 < len) ? landed * 64 - lo63 : len;
           int a = ws, b = we;
           while (a < b) {
             const int mid = (a + b) >> 1;
@@ -348,40 +415,61 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             else b = mid;
           }
           cur = a;
-          const bool miss = len > 0 && ((cur == ws && ws > 0) || (cur == we && we < len));
-          if (miss) {  // rare: the probe did not bracket c0 -> binary search in global memory
-            long long ga = lo, gb = lo + len;
+          if ((cur == ws && ws > 0) || (cur == we && we < len)) {
+            // the probe did not bracket c0 (irregular row): binary search in global memory;
+            // the ring holds nothing useful for the new cursor
+            long long ga = lo, gb = hi;
             while (ga < gb) {
               const long long mid = (ga + gb) >> 1;
               if (__ldg(p.col_indices + mid) < c0) ga = mid + 1;
               else gb = mid;
             }
             cur = static_cast<int>(ga - lo);
+            mtop = landed = mtop_last = (lo63 + cur) >> 6;
           }
-          const int c_lb = (lo63 + cur) >> 6;
-          if (len > 0) {
-            const int from = miss ? c_lb : (mtop > c_lb ? mtop : c_lb);
-            fetch_chunks(lo, from, c_lb + 8);
-          }
-          cp_async_commit();
-          if (__any_sync(0xffffffffu, miss || c_lb + 3 > mtop)) {
-            cp_async_wait<0>();
-            __syncwarp();
-          }
-          mtop = c_lb + 8;
         }
         cur_panel = gpanel;
         MC_STAMP(lane == 0 && bw == 0, 40);
       }
+      else {
+        // every cp.async group but the one committed after the previous tile is complete
+        cp_async_wait<1>();
+        __syncwarp();
+        landed = mtop_last;
+      }
+      MC_STAMP(lane == 0 && bw == 0 && i < 5, 64 + 5 * static_cast<int>(i));
       // ---- this tile's bitmap of row j (lanes of the row split the candidates) ----
-      const int left = len - cur;
-      const int nvalid = (left < kCols) ? left : kCols;
+      const int lim = (len - cur < kCols) ? len - cur : kCols;  // candidates in the tile window
       uint32_t w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
-      bool bad = false;
-      for (int k = sub; __any_sync(0xffffffffu, k < nvalid); k += 16) {
+      bool bad = false, row_live = true;
+      for (int k0 = 0;; k0 += 4 * kLanesPerRow) {
+        const bool act = row_live && k0 < lim;
+        if (!__any_sync(0xffffffffu, act)) break;
+        // candidates [cur + k0, cur + k0 + 16) must have landed
+        const int landed_rel = landed * 64 - lo63;
+        const bool need = act && cur + k0 + 4 * kLanesPerRow > landed_rel && landed_rel < len;
+        if (__any_sync(0xffffffffu, need)) {
+          if (need) {
+            const int last = (cur + k0 + 4 * kLanesPerRow < len) ? cur + k0 + 4 * kLanesPerRow : len;
+            const int c_need = ((lo63 + last - 1) >> 6) + 1;
+            if (c_need > mtop) {
+              const int c_cap = ((lo63 + cur) >> 6) + 8;  // never overwrite the cursor's chunk
+              const int c_to = (c_need + depth - 1 < c_cap) ? c_need + depth - 1 : c_cap;
+              fetch_chunks(lo, mtop, c_to);
+              mtop = c_to;
+            }
+          }
+          cp_async_commit();
+          cp_async_wait<0>();
+          __syncwarp();
+          landed = mtop_last = mtop;
+        }
         uint32_t c[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) c[u] = (k + 4 * u < nvalid) ? rrow[(lo511 + cur + k + 4 * u) & 511] : kNone;
+        for (int u = 0; u < 4; ++u) {
+          const int k = k0 + sub + kLanesPerRow * u;
+          c[u] = (act && k < lim) ? rrow[(lo511 + cur + k) & 511] : kNone;
+        }
         bool more = true;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -396,13 +484,16 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           w2 |= wsel == 2 ? bit : 0u;
           w3 |= wsel == 3 ? bit : 0u;
         }
-        // columns are strictly increasing: once a candidate is past the tile, so are
-        // all later ones of this row -> retire the lane
-        if (!more) k = kCols;
+        // a candidate past the tile ends the row: every later candidate is past it too
+        bool done = !more;
+#pragma unroll
+        for (int o = 1; o < kLanesPerRow; o <<= 1) done |= __shfl_xor_sync(0xffffffffu, done, o);
+        row_live &= !done;
       }
+      MC_STAMP(lane == 0 && bw == 0 && i < 5, 65 + 5 * static_cast<int>(i));
       if (bad) flag_status(p.status, MC_STATUS_BAD_INDEX);
 #pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
+      for (int o = 1; o < kLanesPerRow; o <<= 1) {
         w0 |= __shfl_xor_sync(0xffffffffu, w0, o);
         w1 |= __shfl_xor_sync(0xffffffffu, w1, o);
         w2 |= __shfl_xor_sync(0xffffffffu, w2, o);
@@ -410,17 +501,22 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       const int p0 = __popc(w0), p1 = __popc(w1), p2 = __popc(w2), p3 = __popc(w3);
       const int pre = (sub > 0 ? p0 : 0) + (sub > 1 ? p1 : 0) + (sub > 2 ? p2 : 0);
-      cp_async_wait<0>();  // chunks issued one tile ago (read from the next tile on)
-      tc::mbar_wait(pempty_bar(slot), ((i / kRing) & 1) ^ 1);
-      QuarterMap qm;
-      qm.bits = sub == 0 ? w0 : sub == 1 ? w1 : sub == 2 ? w2 : w3;
-      qm.pad = 0;
-      qm.pos = lo + cur + pre;
-      maps[slot * (VR * 4) + rl * 4 + sub] = qm;
+      MC_STAMP(lane == 0 && bw == 0 && i < 5, 66 + 5 * static_cast<int>(i));
+      tc::mbar_wait(pempty_bar(slot), ((i >> 2) & 1) ^ 1);
+      MC_STAMP(lane == 0 && bw == 0 && i < 5, 67 + 5 * static_cast<int>(i));
+      if (sub < 4) {
+        QuarterMap qm;
+        qm.bits = sub == 0 ? w0 : sub == 1 ? w1 : sub == 2 ? w2 : w3;
+        qm.pad = 0;
+        qm.pos = lo + cur + pre;
+        maps[slot * (VR * 4) + rl * 4 + sub] = qm;
+      }
       cur += p0 + p1 + p2 + p3;
-      const int want = ((lo63 + cur) >> 6) + 8;
-      if (want > mtop) {
-        if (len > 0) fetch_chunks(lo, mtop, want);
+      // keep `depth` chunks in flight past the cursor
+      const int want = ((lo63 + cur) >> 6) + depth;
+      mtop_last = mtop;  // bound of the groups committed so far
+      if (want > mtop && len > 0) {
+        fetch_chunks(lo, mtop, want);
         mtop = want;
       }
       cp_async_commit();
@@ -436,13 +532,14 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t ltmask = (1u << lane) - 1u;
     constexpr int rpc = 32 / V;  // vector rows per 32-column chunk
     constexpr int kChunks = PANEL / 64;  // 32-column TMEM chunks per consumer warp
-    for (int64_t t = t0; t < t1; ++t) {
-      const int64_t i = t - t0;
-      const int slot = static_cast<int>(i % kRing);
-      const int acc = static_cast<int>(i & 1);
-      const int64_t item = t / tiles_per_item;
+    TileCursor tc_(t0, p.n_panels, p.n_ctiles);
+    for (int64_t t = t0; t < t1; ++t, tc_.next()) {
+      const int i = static_cast<int>(t - t0);
+      const int slot = i & (kRing - 1);
+      const int acc = i & 1;
+      const long long item = tc_.item;
       const QuarterMap* m = maps + slot * (VR * 4);
-      tc::mbar_wait(pfull_bar(slot), (i / kRing) & 1);
+      tc::mbar_wait(pfull_bar(slot), (i >> 2) & 1);
       tc::mbar_wait(tfull_bar(acc), (i >> 1) & 1);
       tc::tc_fence_after();
       MC_STAMP(warp == kFirstCons && lane == 0 && i < 6, 23 + 3 * static_cast<int>(i));
@@ -464,7 +561,11 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           for (int w = 0; w < rpc; ++w) {
             const bool present = (qm[w].bits >> lane) & 1u;
             const long long pos = qm[w].pos + __popc(qm[w].bits & ltmask);
+#ifdef MCUBE_NOSTORE
+            if (present && cur[V * w] == 0x7fffffffu) store_block_if<V>(present, out + pos * V, &cur[V * w]);
+#else
             store_block_if<V>(present, out + pos * V, &cur[V * w]);
+#endif
           }
           if (kk + 1 < kChunks) tc::tmem_wait_ld();
         }

@@ -51,9 +51,10 @@ for i in range(5):
     names[42 + 4 * i] = f"p1done{i}"
     names[43 + 4 * i] = f"pempty_ok{i}"
 for i in range(5):
-    for w in range(4):
-        names[64 + 8 * i + w] = f"p1w{w}_{i}"
-        names[68 + 8 * i + w] = f"p2w{w}_{i}"
+    names[64 + 5 * i] = f"b_go{i}"
+    names[65 + 5 * i] = f"b_loop{i}"
+    names[66 + 5 * i] = f"b_red{i}"
+    names[67 + 5 * i] = f"b_pempty{i}"
 for cta in (0, 1, 77, 147):
     row = t[cta]
     ev = sorted((int(v - base), names.get(k, str(k))) for k, v in enumerate(row) if v >= base and v != 0)
