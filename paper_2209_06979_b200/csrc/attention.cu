@@ -166,6 +166,95 @@ __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int6
   }
 }
 
+// ---- fp16-input fast paths (the C4 configuration) ----
+
+// grid (batch * splits, 3): |x| max of a slice of one [L x d] fp16 tensor, combined with an
+// integer atomicMax on the float bit pattern (non-negative floats order like their bits).
+// Exact: the maximum of fp16 magnitudes is representable in fp32.
+__global__ void __launch_bounds__(256)
+absmax_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n, int splits, uint32_t* amax_bits) {
+  const int64_t b = blockIdx.x / splits;
+  const int sp = blockIdx.x - static_cast<int>(b * splits);
+  const int which = blockIdx.y;
+  const __half* src = (which == 0 ? q : (which == 1 ? k : v)) + b * n;
+  const int64_t n8 = n / 8;
+  const int64_t c0 = (n8 * sp) / splits, c1 = (n8 * (sp + 1)) / splits;
+  float m = 0.f;
+  for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(src) + c);
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const float2 f = __half22float2(h[x]);
+      m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
+    }
+  }
+  if (sp == splits - 1)  // tail elements (n not a multiple of 8)
+    for (int64_t i = n8 * 8 + threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, fabsf(__half2float(src[i])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits + b * 3 + which, __float_as_uint(m));
+}
+
+// scales (attention.py:52-54) and the two dequant factors (:147, :169) per head
+__global__ void scales_kernel(const uint32_t* amax_bits, int64_t batch, int bits, int smax, int head_dim,
+                              double* scales, double* alpha_s, double* alpha_m) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const double qmax = static_cast<double>((1 << (bits - 1)) - 1);
+  double sc[3];
+#pragma unroll
+  for (int w = 0; w < 3; ++w) {
+    const double m = static_cast<double>(__uint_as_float(amax_bits[b * 3 + w]));
+    sc[w] = m > 0.0 ? m / qmax : 1.0;
+    scales[b * 4 + w] = sc[w];
+  }
+  const double ss = 1.0 / static_cast<double>(smax);
+  scales[b * 4 + 3] = ss;
+  alpha_s[b] = sc[0] * sc[1] / sqrt(static_cast<double>(head_dim));
+  alpha_m[b] = ss * sc[2];
+}
+
+// 8-bit quantisation of fp16 inputs, 16 elements (one 16-byte output) per thread.
+// FAST: float32 (x / scale rounded half-to-even); otherwise float64 as attention.py:55.
+template <bool FAST>
+__global__ void quant8_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n,
+                                  const double* scales, uint32_t* out, int64_t words_per, int64_t batch) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // 16-element group
+  const int which = blockIdx.y;
+  const int64_t groups = n / 16;
+  if (t >= groups * batch) return;
+  const int64_t b = t / groups, g = t - b * groups;
+  const __half* src = (which == 0 ? q : (which == 1 ? k : v)) + b * n + g * 16;
+  const double scale = scales[b * 4 + which];
+  const float scale_f = static_cast<float>(scale);
+  const uint4 u0 = __ldg(reinterpret_cast<const uint4*>(src)), u1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+  const __half* h = reinterpret_cast<const __half*>(&u0);
+  const __half* h1 = reinterpret_cast<const __half*>(&u1);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const __half x = e < 8 ? h[e] : h1[e - 8];
+    // q = clip(rint(x / scale)) in float64 (attention.py:55). The fp32 quotient is within
+    // 2^-20 relative of it, so it decides rint exactly unless it lies within 2^-12 of a
+    // rounding tie; those (rare) elements take the float64 division.
+    int qi;
+    const float xf = __half2float(x);
+    const float qf = xf / scale_f;
+    const float fr = fabsf(qf - truncf(qf));
+    if (!FAST || fabsf(fr - 0.5f) < 2.4e-4f) {
+      double d = rint(static_cast<double>(xf) / scale);
+      qi = static_cast<int>(fmin(fmax(d, -127.0), 127.0));
+    } else {
+      qi = static_cast<int>(rintf(qf));
+      qi = qi > 127 ? 127 : (qi < -127 ? -127 : qi);
+    }
+    w[e >> 2] |= (static_cast<uint32_t>(qi) & 0xFFu) << (8 * (e & 3));
+  }
+  *reinterpret_cast<uint4*>(out + (static_cast<int64_t>(which) * batch + b) * words_per + g * 4) =
+      make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 }  // namespace
@@ -192,6 +281,7 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
   const size_t o_idx = off; off = align256(off + max_stored * 4);
   const size_t o_idx2 = off; off = align256(off + max_stored * 4);
   const size_t o_sr = off; off = align256(off + B * sr_words * 4);
+  const size_t o_amax = off; off = align256(off + B * 3 * 4);
   if (ws_needed) *ws_needed = off;
   if (!a->workspace) return cudaSuccess;
 
@@ -210,14 +300,40 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
   cudaError_t err;
 
   const int smax = (1 << (sb - 1)) - 1;
-  absmax_kernel<<<dim3(static_cast<unsigned>(B), 3), 512, 0, stream>>>(a->q, a->k, a->v, a->in_dtype, n, qb,
-                                                                       scales, smax);
-  count_launch();
-  quant_kernel<<<dim3(static_cast<unsigned>((B * qwords + 255) / 256), 3), 256, 0, stream>>>(
-      a->q, a->k, a->v, a->in_dtype, n, qb, scales, qkv, qwords, B);
-  count_launch();
-  alpha_kernel<<<static_cast<unsigned>((B + 127) / 128), 128, 0, stream>>>(scales, B, a->head_dim, alpha_s, alpha_m);
-  count_launch();
+  const bool fast = a->mode == MC_ATTN_FAST;
+  if (a->in_dtype == MC_DTYPE_F16 && qb == 8 && n % 16 == 0 && (reinterpret_cast<uintptr_t>(a->q) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(a->k) & 15) == 0 && (reinterpret_cast<uintptr_t>(a->v) & 15) == 0) {
+    // vectorised fp16 path: split absmax (atomicMax on float bits) -> scales -> 16-wide quant
+    uint32_t* amax = reinterpret_cast<uint32_t*>(ws + o_amax);
+    cudaMemsetAsync(amax, 0, B * 3 * 4, stream);
+    const int splits = static_cast<int>(n / 8 >= 8 * 256 ? 8 : 1);
+    absmax_f16_kernel<<<dim3(static_cast<unsigned>(B * splits), 3), 256, 0, stream>>>(
+        static_cast<const __half*>(a->q), static_cast<const __half*>(a->k), static_cast<const __half*>(a->v), n, splits,
+        amax);
+    count_launch();
+    scales_kernel<<<static_cast<unsigned>((B + 127) / 128), 128, 0, stream>>>(amax, B, qb, smax, a->head_dim, scales,
+                                                                             alpha_s, alpha_m);
+    count_launch();
+    const unsigned qgrid = static_cast<unsigned>((B * (n / 16) + 255) / 256);
+    if (fast)
+      quant8_f16_kernel<true><<<dim3(qgrid, 3), 256, 0, stream>>>(
+          static_cast<const __half*>(a->q), static_cast<const __half*>(a->k), static_cast<const __half*>(a->v), n,
+          scales, qkv, qwords, B);
+    else
+      quant8_f16_kernel<false><<<dim3(qgrid, 3), 256, 0, stream>>>(
+          static_cast<const __half*>(a->q), static_cast<const __half*>(a->k), static_cast<const __half*>(a->v), n,
+          scales, qkv, qwords, B);
+    count_launch();
+  } else {
+    absmax_kernel<<<dim3(static_cast<unsigned>(B), 3), 512, 0, stream>>>(a->q, a->k, a->v, a->in_dtype, n, qb,
+                                                                         scales, smax);
+    count_launch();
+    quant_kernel<<<dim3(static_cast<unsigned>((B * qwords + 255) / 256), 3), 256, 0, stream>>>(
+        a->q, a->k, a->v, a->in_dtype, n, qb, scales, qkv, qwords, B);
+    count_launch();
+    alpha_kernel<<<static_cast<unsigned>((B + 127) / 128), 128, 0, stream>>>(scales, B, a->head_dim, alpha_s, alpha_m);
+    count_launch();
+  }
 
   // mask -> SR-BCRS structure of the probability matrix (stride = plan tile k)
   if ((err = launch_srbcrs_plan(a->mask->row_offsets, vrows, S, sr_begin, sr_end, sr_total, stream)) != cudaSuccess)
@@ -242,11 +358,12 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
   sp.out = a->scores_int; sp.out_stride = nblk * 8;
   sp.alpha = alpha_s; sp.out_f16 = scores; sp.f16_stride = nblk * 8;
   sp.status = status;
+  sp.f16_fast = 0;  // fp16(acc * alpha) rounded from float64 in both modes (exact)
   if ((err = launch_sddmm(sp, stream)) != cudaSuccess) return err;
 
   const int64_t warps = B * vrows;
   const unsigned grid = static_cast<unsigned>((warps * 32 + 255) / 256);
-  if (a->mode == MC_ATTN_FAST)
+  if (fast)
     softmax_requant_kernel<true><<<grid, 256, 0, stream>>>(scores, nblk * 8, a->mask->row_offsets, vrows, sr_begin, S,
                                                            smax, sb, sr_vals, sr_words, a->probs_f16, a->probs_int, B);
   else

@@ -144,4 +144,17 @@ __device__ __forceinline__ uint16_t f16_bits_rn(double x) {
   return *reinterpret_cast<uint16_t*>(&h);
 }
 
+// fp16(round_to_nearest((double)acc * alpha)) -- the reference's dequant rounding chain
+// (attention.py:62-65, :149-153, :170-173) -- evaluated in fp32 whenever fp32 decides it:
+// the fp32 product is within 4 * 2^-24 relative of the float64 one, so if scaling it by
+// 1 -/+ 2^-21 rounds to the same fp16 value the float64 product does too; otherwise (a
+// product next to an fp16 rounding boundary, ~1e-3 of the cases) take float64.
+__device__ __forceinline__ uint16_t f16_dequant(int32_t acc, double alpha, float alpha_f) {
+  const float y = static_cast<float>(acc) * alpha_f;
+  const uint16_t lo = __half_as_ushort(__float2half_rn(y * 0.99999952316284180f));
+  const uint16_t hi = __half_as_ushort(__float2half_rn(y * 1.00000047683715820f));
+  if (lo == hi) return lo;
+  return f16_bits_rn(static_cast<double>(acc) * alpha);
+}
+
 }  // namespace mcube

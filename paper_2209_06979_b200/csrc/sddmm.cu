@@ -107,6 +107,7 @@ sddmm_kernel(const SddmmParams p) {
   const bool a_ok = g < V;
   double alpha = 0.0;
   if (p.out_f16) alpha = p.alpha ? p.alpha[b] : p.alpha_host;
+  const float alpha_f = static_cast<float>(alpha);
   bool overflow = false;
 
   for (int64_t gi = gbeg; gi < gend; ++gi) {
@@ -188,7 +189,7 @@ sddmm_kernel(const SddmmParams p) {
         overflow |= !fits_i32(total);
         const int64_t o = (blk0 + m) * V + v;
         if (p.out) p.out[b * p.out_stride + o] = static_cast<int32_t>(total);
-        if (p.out_f16) p.out_f16[b * p.f16_stride + o] = f16_bits_rn(static_cast<double>(total) * alpha);
+        if (p.out_f16) p.out_f16[b * p.f16_stride + o] = f16_dequant(static_cast<int32_t>(total), alpha, alpha_f);
       }
     }
   }
@@ -234,7 +235,9 @@ static int sddmm_path_override() {
 cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream) {
   const int ov = sddmm_path_override();
   const double density = (p.M > 0 && p.N > 0) ? static_cast<double>(p.n_blocks) * p.V / (static_cast<double>(p.M) * p.N) : 0.0;
-  if (ov != 2 && sddmm_tc_supported(p) && (ov == 1 || density >= 0.08)) return launch_sddmm_tc(p, stream);
+  // K = 64 (attention heads, d = 64) stays on the gather kernel by default: with only two
+  // K-steps per tile the dense path is bound by draining the whole accumulator tile.
+  if (ov != 2 && sddmm_tc_supported(p) && (ov == 1 || (density >= 0.08 && p.K >= 128))) return launch_sddmm_tc(p, stream);
   // warps per vector row: about one group of 16 blocks each
   const double avg_groups = p.vrows ? (static_cast<double>(p.n_blocks) / p.vrows) / 16.0 : 0.0;
   int splits = static_cast<int>(avg_groups + 0.999);

@@ -172,7 +172,9 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int KB = static_cast<int>(p.K / 128);
+  // K is staged in blocks of KBLK bytes: 128 (SWIZZLE_128B, K = 128/256) or 64 (SWIZZLE_64B, K = 64)
+  const int KBLK = p.K >= 128 ? 128 : 64;
+  const int KB = static_cast<int>(p.K / KBLK);
   QuarterMap* maps = reinterpret_cast<QuarterMap*>(smem + L::OFF_MAP);
   const uint32_t bar0 = sbase + L::OFF_BAR;
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
@@ -286,9 +288,9 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const long long item = tc_.item, panel = tc_.panel, ct = tc_.ct, gpanel = tc_.gpanel;
         if (gpanel != cur_panel) {
           if (n_a > 0) tc::mbar_wait(a_empty, (n_a - 1) & 1);
-          tc::mbar_arrive_expect_tx(a_full, KB * PANEL * 128);
+          tc::mbar_arrive_expect_tx(a_full, KB * PANEL * KBLK);
           for (int kb = 0; kb < KB; ++kb)
-            tc::tma_load_2d(sbase + L::OFF_A + kb * PANEL * 128, &tmA, a_full, kb * 128,
+            tc::tma_load_2d(sbase + L::OFF_A + kb * PANEL * KBLK, &tmA, a_full, kb * KBLK,
                             static_cast<int>(item * p.M + panel * PANEL));
           ++n_a;
           cur_panel = gpanel;
@@ -296,9 +298,9 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int s = static_cast<int>(i % kStages);
         const uint32_t u = static_cast<uint32_t>(i / kStages);
         tc::mbar_wait(empty_bar(s), (u & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(full_bar(s), KB * kCols * 128);
+        tc::mbar_arrive_expect_tx(full_bar(s), KB * kCols * KBLK);
         for (int kb = 0; kb < KB; ++kb)
-          tc::tma_load_2d(sbase + L::OFF_B + s * L::B_STAGE + kb * kCols * 128, &tmB, full_bar(s), kb * 128,
+          tc::tma_load_2d(sbase + L::OFF_B + s * L::B_STAGE + kb * kCols * KBLK, &tmB, full_bar(s), kb * KBLK,
                           static_cast<int>(item * p.N + ct * kCols));
         MC_STAMP(i < 6, 2 + static_cast<int>(i));
       }
@@ -328,10 +330,13 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const uint32_t d = tmem + acc * PANEL;
         const uint32_t bs = sbase + L::OFF_B + s * L::B_STAGE;
         const uint32_t as = sbase + L::OFF_A;
-        for (int ks = 0; ks < KB * 4; ++ks) {
-          const int kb = ks >> 2, off = (ks & 3) * 32;
-          const uint64_t adesc = tc::desc_k_sw128(bs + kb * kCols * 128 + off);   // B^T tile: M = 128
-          const uint64_t bdesc = tc::desc_k_sw128(as + kb * PANEL * 128 + off);  // A panel:  N = PANEL
+        const int kpb = KBLK / 32;  // K=32 MMA steps per staged block
+        for (int ks = 0; ks < KB * kpb; ++ks) {
+          const int kb = ks / kpb, off = (ks % kpb) * 32;
+          const uint32_t aaddr = bs + kb * kCols * KBLK + off;  // B^T tile: M = 128
+          const uint32_t baddr = as + kb * PANEL * KBLK + off;  // A panel:  N = PANEL
+          const uint64_t adesc = KBLK == 128 ? tc::desc_k_sw128(aaddr) : tc::desc_k_sw64(aaddr);
+          const uint64_t bdesc = KBLK == 128 ? tc::desc_k_sw128(baddr) : tc::desc_k_sw64(baddr);
           tc::mma_i8(d, adesc, bdesc, kIdesc, ks > 0 ? 1u : 0u);
         }
         tc::mma_commit(empty_bar(s));
@@ -570,22 +575,32 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           if (kk + 1 < kChunks) tc::tmem_wait_ld();
         }
       } else {
-        // fused dequant epilogue (attention.py:149-153): int32 (optional) + fp16(acc * alpha)
+        // fused dequant epilogue (attention.py:147-154): fp16(acc * alpha) per block as one
+        // V*2-byte store (+ the int32 accumulators when requested), rounded exactly as the
+        // reference's float64 product (f16_dequant).
         int32_t* out = p.out ? p.out + item * p.out_stride : nullptr;
         uint16_t* out16 = p.out_f16 + item * p.f16_stride;
         const double alpha = p.alpha ? p.alpha[item] : p.alpha_host;
+        const float alpha_f = static_cast<float>(alpha);
+#pragma unroll 1
         for (int kk = 0; kk < kChunks; ++kk) {
           if (kk > 0) tc::tmem_ld32(tl + 32 * kk, va);
+#pragma unroll
           for (int w = 0; w < rpc; ++w) {
             const QuarterMap qm = m[((kChunks * half + kk) * rpc + w) * 4 + q];
-            if ((qm.bits >> lane) & 1u) {
-              const long long pos = qm.pos + __popc(qm.bits & ltmask);
-              uint32_t v[V];
+            const bool present = (qm.bits >> lane) & 1u;
+            const long long pos = qm.pos + __popc(qm.bits & ltmask);
+            if (out) store_block_if<V>(present, out + pos * V, &va[V * w]);
+            uint32_t h2[V / 2];
 #pragma unroll
-              for (int x = 0; x < V; ++x) v[x] = va[V * w + x];
-              if (out) store_block_if<V>(true, out + pos * V, v);
-#pragma unroll
-              for (int x = 0; x < V; ++x) out16[pos * V + x] = f16_bits_rn(static_cast<double>(static_cast<int32_t>(v[x])) * alpha);
+            for (int x = 0; x < V / 2; ++x) {
+              const int32_t a0 = static_cast<int32_t>(va[V * w + 2 * x]), a1 = static_cast<int32_t>(va[V * w + 2 * x + 1]);
+              const uint16_t l = f16_dequant(a0, alpha, alpha_f), h = f16_dequant(a1, alpha, alpha_f);
+              h2[x] = static_cast<uint32_t>(l) | (static_cast<uint32_t>(h) << 16);
+            }
+            if (present) {
+              if constexpr (V == 8) *reinterpret_cast<uint4*>(out16 + pos * V) = make_uint4(h2[0], h2[1], h2[2], h2[3]);
+              else *reinterpret_cast<uint2*>(out16 + pos * V) = make_uint2(h2[0], h2[1]);
             }
           }
         }
@@ -627,13 +642,14 @@ EncodeFn encode_fn() {
 bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t kbytes, int box_rows) {
   EncodeFn fn = encode_fn();
   if (!fn) return false;
+  const int kblk = kbytes >= 128 ? 128 : 64;  // 128-byte (SW128) or 64-byte (SW64) K blocks
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(kbytes), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(kbytes)};
-  cuuint32_t box[2] = {128, static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kblk), static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            CU_TENSOR_MAP_INTERLEAVE_NONE, kblk == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace
@@ -641,7 +657,8 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t kbytes, in
 bool sddmm_tc_supported(const SddmmParams& p) {
   const bool dense_items = p.batch == 1 || (p.a_stride * 4 == p.M * p.K && p.b_stride * 4 == p.N * p.K);
   const uintptr_t out_align = static_cast<uintptr_t>(4 * p.V);
-  return p.LB == 8 && p.RB == 8 && (p.V == 4 || p.V == 8) && (p.K == 128 || p.K == 256) &&
+  return p.LB == 8 && p.RB == 8 && (p.V == 4 || p.V == 8) && (p.K == 64 || p.K == 128 || p.K == 256) &&
+         (p.out_f16 == nullptr || (reinterpret_cast<uintptr_t>(p.out_f16) % (2 * p.V)) == 0) &&
          p.batch >= 1 && dense_items && (p.out != nullptr || p.out_f16 != nullptr) &&
          (p.out == nullptr || ((reinterpret_cast<uintptr_t>(p.out) % out_align) == 0 && (p.out_stride % p.V) == 0)) &&
          (reinterpret_cast<uintptr_t>(p.a_words) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.b_words) & 15) == 0 &&
@@ -667,6 +684,7 @@ cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream) {
   q.alpha = p.alpha;
   q.alpha_host = p.alpha_host;
   q.out_f16 = p.out_f16;
+  q.f16_fast = p.f16_fast;
   q.f16_stride = p.f16_stride;
   q.status = p.status;
   q.n_panels = static_cast<int>((p.M + kVRows * p.V - 1) / (kVRows * p.V));

@@ -385,6 +385,7 @@ spmm_kernel(const SpmmParams p) {
 
   double alpha = 0.0;
   if (p.out_f16) alpha = p.alpha ? p.alpha[b] : p.alpha_host;
+  const float alpha_f = static_cast<float>(alpha);
   const int64_t row0 = r * V;
 #pragma unroll
   for (int vv = 0; vv < 2; ++vv) {
@@ -413,7 +414,7 @@ spmm_kernel(const SpmmParams p) {
       uint16_t* o = p.out_f16 + b * p.f16_stride + base;
 #pragma unroll
       for (int x = 0; x < 8; ++x)
-        if (n0 + x < p.N) o[x] = f16_bits_rn(static_cast<double>(rowv[x]) * alpha);
+        if (n0 + x < p.N) o[x] = f16_dequant(rowv[x], alpha, alpha_f);
     }
   }
 }

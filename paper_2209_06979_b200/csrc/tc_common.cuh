@@ -113,6 +113,11 @@ __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
 }
 
+// UMMA shared-memory descriptor: K-major, 64-byte swizzle (64-byte rows), 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t desc_k_sw64(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (1ull << 16) | (32ull << 32) | (1ull << 46) | (4ull << 61);
+}
+
 // Instruction descriptor for kind::i8: s32 accumulate, s8 x s8, both K-major.
 constexpr uint32_t idesc_i8(int m, int n, bool a_unsigned = false, bool b_unsigned = false) {
   return (2u << 4) | ((a_unsigned ? 0u : 1u) << 7) | ((b_unsigned ? 0u : 1u) << 10) |

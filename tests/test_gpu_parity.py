@@ -240,7 +240,7 @@ def test_c3_full_size_rows_subset():
 @pytest.mark.parametrize("path", ["dense", "gather"])
 @pytest.mark.parametrize("v", [2, 4, 8])
 @pytest.mark.parametrize("shape", [(512, 512, 256, 0.5), (1024, 640, 128, 0.9), (264, 300, 256, 0.7),
-                                   (256, 128, 256, 0.98)])
+                                   (256, 128, 256, 0.98), (768, 512, 64, 0.8)])
 def test_sddmm_paths_vs_oracle(path, v, shape, monkeypatch):
     m, n, k, sp = shape
     monkeypatch.setenv("MCUBE_SDDMM_PATH", path)
