@@ -140,6 +140,7 @@ int mc_spmm_batched(const mc_srbcrs* lhs, int64_t lhs_words_stride, const mc_den
   p.batch = batch;
   p.row_begin = lhs->row_begin;
   p.row_end = lhs->row_end;
+  p.stored = lhs->stored_vectors;
   p.col_indices = lhs->col_indices;
   p.lhs_words = lhs->words;
   p.lhs_stride = lhs_words_stride;

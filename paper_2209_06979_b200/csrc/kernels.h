@@ -25,6 +25,7 @@ struct SpmmParams {
   uint16_t* out_f16;
   int64_t f16_stride;
   uint32_t* status;
+  int64_t stored;  // stored vectors per batch item (SR-BCRS col_indices length); 0 = unknown
   // filled by the launcher
   int64_t ntiles, tasks;
 };
@@ -69,6 +70,9 @@ struct SddmmTcParams {
 };
 
 cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream);
+// tcgen05 gather path (spmm_tc.cu); launch_spmm dispatches to it when supported
+bool spmm_tc_supported(const SpmmParams& p);
+cudaError_t launch_spmm_tc(SpmmParams p, cudaStream_t stream);
 cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream);
 // dense-tile tcgen05 path (sddmm_tc.cu); launch_sddmm dispatches to it by density
 bool sddmm_tc_supported(const SddmmParams& p);

@@ -452,6 +452,7 @@ cudaError_t launch_spmm_lr(const SpmmParams& p, cudaStream_t stream) {
 }  // namespace
 
 cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream) {
+  if (spmm_tc_supported(p)) return launch_spmm_tc(p, stream);
   p.ntiles = (p.N + kTileN - 1) / kTileN;
   p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.ntiles;
   const int key = p.LB * 100 + p.RB;

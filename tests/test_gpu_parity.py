@@ -356,3 +356,42 @@ def test_sddmm_dense_batched_with_f16_epilogue(v, monkeypatch):
         assert (got[i] == want).all(), i
         w16 = (want.astype(np.float64) * float(alpha[i])).astype(np.float16)
         assert (got16[i].view(np.uint16) == w16.view(np.uint16)).all(), i
+
+
+# ---------------- tcgen05 SpMM path (gather4 + MN-major UMMA) vs the oracle ----------------
+
+def _spmm_irregular(m, k, v, seed, stride):
+    """SR-BCRS with empty, full, clustered and random rows (8-bit values)."""
+    rng = np.random.default_rng(seed)
+    offs, cols = _irregular_pattern(m, k, v, seed)
+    vals = rng.integers(-127, 128, size=cols.size * v)
+    vals[vals == 0] = 1
+    begin, end, sidx, svals = O.srbcrs_from_bcrs(offs, cols, vals, v, stride)
+    return begin, end, sidx, svals
+
+
+@pytest.mark.parametrize("path", ["tc", "mma"])
+@pytest.mark.parametrize("shape", [(512, 256, 512, 0.9, 1), (1024, 384, 2048, 0.7, 1), (256, 512, 4096, 0.98, 2),
+                                   (768, 144, 1024, 0.5, 4)])
+def test_spmm_l8r8_paths_vs_oracle(path, shape, monkeypatch):
+    m, n, k, sp, smult = shape
+    monkeypatch.setenv("MCUBE_SPMM_PATH", path)
+    c = O.build_spmm_case(m, n, k, 8, sp, 8, 8, seed=m + n + smult, stride_mult=smult)
+    lhs = mc.SrBcrsMatrix(m, k, 8, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                          mc.PackedArray.from_values(c["values"], 8))
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], 8)))
+    want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], 8, c["stride"], False,
+                  8, c["rhs"], 8, n)
+    assert (np.asarray(out) == want).all()
+
+
+@pytest.mark.parametrize("stride", [16, 32])
+def test_spmm_tc_irregular_rows(stride):
+    m, n, k = 640, 256, 1536
+    begin, end, sidx, svals = _spmm_irregular(m, k, 8, 5 + stride, stride)
+    rng = np.random.default_rng(9)
+    rhs = rng.integers(-127, 128, size=(k, n))
+    lhs = mc.SrBcrsMatrix(m, k, 8, stride, begin, end, sidx, mc.PackedArray.from_values(svals, 8))
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(rhs, 8)))
+    want = O.spmm(begin, end, sidx, svals, 8, stride, False, 8, rhs, 8, n)
+    assert (np.asarray(out) == want).all()

@@ -1,6 +1,6 @@
 """SpMM throughput on B200 for BASELINE configs C1, C3 (grid) and C5 (CUDA-graph timing, cold L2).
 
-usage: python tools/bench_spmm.py [c1] [c3] [c3full] [c5] [--out file.json]
+usage: python tools/bench_spmm.py [c1] [c3l8] [c3] [c3full] [c5] [--out file.json]
 
 Per cell: inputs from the reference generators (oracle.build_spmm_case semantics:
 generate_synthetic + bcrs_to_srbcrs + shuffle for R4, bench.py:93-110), resident on
@@ -103,6 +103,12 @@ def main():
     if "c1" in args:
         seed = O.cell_seed(0, ((512, 256, 512), 8, 0.9, "L8-R8"))
         res.append(dict(cfg="C1", **cell(512, 256, 512, 8, 0.9, 8, 8, seed, flush)))
+    if "c3l8" in args:  # the tcgen05 path's cells: L8-R8, V=8
+        for sp in (0.7, 0.9, 0.98):
+            seed = O.cell_seed(0, ((4096, 512, 4096), 8, sp, "L8-R8"))
+            r = dict(cfg="C3", **cell(4096, 512, 4096, 8, sp, 8, 8, seed, flush))
+            res.append(r)
+            print(json.dumps(r), flush=True)
     if "c3" in args or "c3full" in args:
         sps = (0.7, 0.8, 0.9, 0.95, 0.98) if "c3full" in args else (0.7, 0.9, 0.98)
         for lb, rb in PAIRS:
