@@ -26,6 +26,7 @@ struct SpmmParams {
   int64_t f16_stride;
   uint32_t* status;
   int64_t stored;  // stored vectors per batch item (SR-BCRS col_indices length); 0 = unknown
+  int gather_tma;  // tcgen05 path: stage gathered rows with TMA gather4 instead of cp.async
   // filled by the launcher
   int64_t ntiles, tasks;
 };

@@ -15,13 +15,15 @@
 // check_accumulation_bound, emulation.py:108-113, guarantees K*(2^8-1)^2 < 2^31).
 // Sentinel / padding slots (sparse_format.py:25) gather row -1: TMA zero-fills it.
 //
-// CTA (192 threads; several CTAs per SM):
-//   warp 0    producer: per task, bulk-copies the row's column indices (1024-entry chunks,
-//             double buffered) and per k-step issues 8 gather4 + 1 stride-block load into
-//             a kStages ring (mbarrier transaction counts);
-//   warp 1    TMEM allocator + single-thread MMA issuer (one tcgen05.mma per k-step,
+// CTA (288 threads; several CTAs per SM):
+//   warps 0-3 producers (k-steps dealt round-robin): per task the row's column indices are
+//             bulk-copied (1024-entry chunks, double buffered); per k-step the warp copies
+//             the 32 gathered rows (8 lanes per 128-byte row, coalesced cp.async) into the
+//             swizzled operand layout plus the stride blocks, arriving on the step's
+//             mbarrier through cp.async.mbarrier.arrive;
+//   warp 4    TMEM allocator + single-thread MMA issuer (one tcgen05.mma per k-step,
 //             kAcc accumulators in flight so a task's MMAs overlap the previous drain);
-//   warps 2-5 epilogue: tcgen05.ld of the 8 accumulator columns of lane quarter q, then
+//   warps 5-8 epilogue: tcgen05.ld of the 8 accumulator columns of lane quarter q, then
 //             coalesced 128-byte stores of each output row (optional fused fp16 dequant).
 #include <cuda_fp16.h>
 
@@ -35,13 +37,15 @@ namespace mcube {
 namespace {
 
 constexpr int kNT = 128;       // dense columns per task (UMMA M)
-constexpr int kStages = 8;     // k-step ring depth
 constexpr int kAcc = 4;        // TMEM accumulators (8 columns each)
 constexpr int kIdxChunk = 1024;
-constexpr int kThreads = 192;
+constexpr int kProd = 4;        // producer warps (k-steps dealt round-robin)
+constexpr int kMmaWarp = kProd;  // then the MMA warp, then 4 epilogue warps
+constexpr int kThreads = 32 * (kProd + 1 + 4);
 constexpr int kATile = 32 * kNT;  // 4 KB: 32 gathered rows x 128 bytes
 constexpr int kLTile = 256;       // 8 rows x 32 bytes of LHS values
 
+template <int kStages>
 struct SmemL {
   static constexpr int OFF_A = 0;                                  // kStages x 4 KB (1024-aligned)
   static constexpr int OFF_L = OFF_A + kStages * kATile;           // kStages x 256 B
@@ -118,27 +122,28 @@ struct TaskCursor {  // task t -> (batch item, vector row, column tile), advance
   }
 };
 
+template <int kStages>
 __global__ void __launch_bounds__(kThreads)
 spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmL, const SpmmParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t bar0 = sbase + SmemL::OFF_BAR;
+  const uint32_t bar0 = sbase + SmemL<kStages>::OFF_BAR;
   auto full_bar = [&](int s) { return bar0 + 8 * s; };
   auto empty_bar = [&](int s) { return bar0 + 8 * (kStages + s); };
   auto tfull_bar = [&](int a) { return bar0 + 8 * (2 * kStages + a); };
   auto tempty_bar = [&](int a) { return bar0 + 8 * (2 * kStages + kAcc + a); };
   auto idx_bar = [&](int b) { return bar0 + 8 * (2 * kStages + 2 * kAcc + b); };
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + SmemL::OFF_TMEM);
-  const uint32_t* idx_s = reinterpret_cast<const uint32_t*>(smem + SmemL::OFF_IDX);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + SmemL<kStages>::OFF_TMEM);
+  const uint32_t* idx_s = reinterpret_cast<const uint32_t*>(smem + SmemL<kStages>::OFF_IDX);
   const long long tasks = p.tasks;
   const long long stride = gridDim.x;
   const int S = p.S;
 
-  if (warp == 0 && lane == 0) {
+  if (warp == kMmaWarp && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
-      tc::mbar_init(full_bar(s), 32);  // one cp.async-completion arrival per producer lane
+      tc::mbar_init(full_bar(s), p.gather_tma ? 1 : 32);  // TMA: tx bytes; cp.async: one arrival per lane
       tc::mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < kAcc; ++a) {
@@ -151,14 +156,15 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
     tc::prefetch_tmap(&tmB);
     tc::prefetch_tmap(&tmL);
   }
-  if (warp == 1) tc::tmem_alloc<32>(smem_u32(tmem_holder));
+  if (warp == kMmaWarp) tc::tmem_alloc<32>(smem_u32(tmem_holder));
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp == 0) {
-    // ---------------- producer ----------------
+  if (warp < kProd) {
+    // ---------------- producers ----------------
+    const int pw = warp;
     const bool shuffled = p.shuffled != 0;
     // value position -> stored index position within an 8-group (sparse_format.py:222-230)
     const int kperm = shuffled ? ((lane & ~7) | (((lane & 7) >> 1) | ((lane & 1) << 2))) : lane;
@@ -170,9 +176,9 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
     uint32_t nchunk = 0;  // index chunks consumed so far (buffer = nchunk & 1)
     // index chunk (pb + c0, cn) -> buffer b; lane 0 issues
     auto load_chunk = [&](uint32_t b, long long src, int cn) {
-      if (lane == 0) {
+      if (pw == 0 && lane == 0) {
         tc::mbar_arrive_expect_tx(idx_bar(b), cn * 4);
-        bulk_load(sbase + SmemL::OFF_IDX + b * kIdxChunk * 4, p.col_indices + src, cn * 4, idx_bar(b));
+        bulk_load(sbase + SmemL<kStages>::OFF_IDX + b * kIdxChunk * 4, p.col_indices + src, cn * 4, idx_bar(b));
       }
     };
     TaskCursor tcur(blockIdx.x, p.vrows, p.ntiles);
@@ -200,6 +206,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
       for (int c0 = 0; c0 < stored; c0 += kIdxChunk) {
         const int cn = (stored - c0 < kIdxChunk) ? stored - c0 : kIdxChunk;
         const uint32_t buf = nchunk & 1;
+        // every producer is done with the previous chunk: its buffer may be refilled
+        tc::named_bar(1, 32 * kProd);
         // prefetch the following chunk (this task's next one, or the next task's first)
         if (c0 + kIdxChunk < stored) {
           const int cn2 = (stored - c0 - kIdxChunk < kIdxChunk) ? stored - c0 - kIdxChunk : kIdxChunk;
@@ -213,14 +221,42 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
         const uint32_t* ix = idx_s + buf * kIdxChunk;
         const int s_end = (c0 + cn + 31) >> 5;
         for (int s = c0 >> 5; s < s_end; ++s, ++g) {
+          if (static_cast<int>(g % kProd) != pw) continue;  // this warp's k-steps
           const int q = 32 * s + lane;  // value position of this lane's k slot (= A-operand row k)
+          const int slot = g % kStages;
+          if (p.gather_tma) {
+            // TMA: 8 x gather4 (4 rows of 128 B each, 128-byte swizzle applied by the TMA unit)
+            // + one 2-D box of stride blocks; completion counted in bytes on the step barrier
+            int row = -1;
+            if (q < stored) {
+              const uint32_t col = ix[(32 * s + kperm) - c0];
+              if (col < kdim) row = static_cast<int>(brow0 + col);
+              else if (col != kSentinel) flag_status(p.status, MC_STATUS_BAD_INDEX);
+            }
+            tc::mbar_wait(empty_bar(slot), ((g / kStages) & 1) ^ 1);
+            if (lane == 0) tc::mbar_arrive_expect_tx(full_bar(slot), kATile + kLTile);
+            __syncwarp();
+            const int r0 = __shfl_sync(0xffffffffu, row, (4 * lane) & 31);
+            const int r1 = __shfl_sync(0xffffffffu, row, (4 * lane + 1) & 31);
+            const int r2 = __shfl_sync(0xffffffffu, row, (4 * lane + 2) & 31);
+            const int r3 = __shfl_sync(0xffffffffu, row, (4 * lane + 3) & 31);
+            const uint32_t adst = sbase + SmemL<kStages>::OFF_A + slot * kATile;
+            if (lane < 8) tma_gather4(adst + lane * 512, &tmB, full_bar(slot), col_byte, r0, r1, r2, r3);
+            if (lane == 8) {
+              const uint32_t ldst = sbase + SmemL<kStages>::OFF_L + slot * kLTile;
+              if (S == 16) tc::tma_load_2d(ldst, &tmL, full_bar(slot), 0, static_cast<int>(lrow0 + 16 * s));
+              else
+                tc::tma_load_2d(ldst, &tmL, full_bar(slot), (32 * s) % S,
+                                static_cast<int>(lrow0 + ((32 * s) / S) * 8));
+            }
+            continue;
+          }
           const uint8_t* src = nullptr;
           if (q < stored) {
             const uint32_t col = ix[(32 * s + kperm) - c0];
             if (col < kdim) src = rhs_b + (brow0 + col) * p.N + col_byte;
             else if (col != kSentinel) flag_status(p.status, MC_STATUS_BAD_INDEX);
           }
-          const int slot = g % kStages;
           tc::mbar_wait(empty_bar(slot), ((g / kStages) & 1) ^ 1);
           // row k of the MN-major SW128 operand: 8-row group k/8 (1024 B), row k%8 (128 B),
           // 16-byte chunk c stored at chunk c ^ (k % 8); a sentinel row is zero-filled.
@@ -233,23 +269,23 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
             const uint8_t* rs = reinterpret_cast<const uint8_t*>(
                 __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), k));
             const bool ok = rs != nullptr && col_ok;
-            const uint32_t dst = sbase + SmemL::OFF_A + slot * kATile + (k >> 3) * 1024 + (k & 7) * 128 +
+            const uint32_t dst = sbase + SmemL<kStages>::OFF_A + slot * kATile + (k >> 3) * 1024 + (k & 7) * 128 +
                                  ((c ^ (k & 7)) << 4);
             cp_async16(dst, ok ? rs + 16 * c : rhs_b, ok ? 16u : 0u);
           }
           // the k-step's stride blocks: S = 16 -> two 8 x 16 B core matrices (plain copy);
           // S % 32 == 0 -> 8 rows x 32 B with the 32-byte swizzle (chunk ^= (row >> 2) & 1)
           if (lane < 16) {
-            const uint32_t ldst = sbase + SmemL::OFF_L + slot * kLTile;
+            const uint32_t ldst = sbase + SmemL<kStages>::OFF_L + slot * kLTile;
             const uint8_t* lsrc;
             uint32_t loff;
             if (S == 16) {
               lsrc = lhs_b + (lrow0 + 16 * s) * 16 + 16 * lane;
               loff = 16 * lane;
             } else {
-              const int v = lane >> 1, c = lane & 1;
-              lsrc = lhs_b + (lrow0 + ((32 * s) / S) * 8 + v) * S + (32 * s) % S + 16 * c;
-              loff = v * 32 + ((c ^ ((v >> 2) & 1)) << 4);
+              const int v = lane >> 1, cc = lane & 1;
+              lsrc = lhs_b + (lrow0 + ((32 * s) / S) * 8 + v) * S + (32 * s) % S + 16 * cc;
+              loff = v * 32 + ((cc ^ ((v >> 2) & 1)) << 4);
             }
             // (the second stride of a row's last S = 16 step may lie past the array end)
             const bool in = lsrc < lhs_end;
@@ -263,7 +299,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
       pb = npb;
       n_true = nend - npb;
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint32_t idesc = tc::idesc_i8(128, 8) | (1u << 15);  // A (gathered rows) MN-major
@@ -285,8 +321,8 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
           tc::mbar_wait(full_bar(slot), (g / kStages) & 1);
           tc::fence_proxy_async();  // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
           tc::tc_fence_after();
-          const uint32_t a_addr = sbase + SmemL::OFF_A + slot * kATile;
-          const uint32_t l_addr = sbase + SmemL::OFF_L + slot * kLTile;
+          const uint32_t a_addr = sbase + SmemL<kStages>::OFF_A + slot * kATile;
+          const uint32_t l_addr = sbase + SmemL<kStages>::OFF_L + slot * kLTile;
           const uint64_t adesc = desc_mn_sw128(a_addr);
           const uint64_t bdesc = S == 16 ? desc_k_interleave(l_addr) : desc_k_sw32(l_addr);
           tc::mma_i8(d, adesc, bdesc, idesc, s > 0 ? 1u : 0u);
@@ -297,7 +333,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5 -> TMEM lane quarters 2,3,0,1) ----------------
+    // ---------------- epilogue (warps 5..8 -> TMEM lane quarters 1,2,3,0) ----------------
     const int q = warp & 3;
     int i = 0;
     TaskCursor tcur(blockIdx.x, p.vrows, p.ntiles);
@@ -340,7 +376,7 @@ spmm_tc_kernel(const __grid_constant__ CUtensorMap tmB, const __grid_constant__ 
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kMmaWarp) {
     tc::tc_fence_after();
     tc::tmem_dealloc<32>(tmem);
   }
@@ -378,8 +414,10 @@ bool encode2d(CUtensorMap* m, const void* base, uint64_t inner_bytes, uint64_t r
 }  // namespace
 
 bool spmm_tc_supported(const SpmmParams& p) {
+  // Opt-in (MCUBE_SPMM_PATH=tc): on C3 this path matches the mma.sync kernel at 70% sparsity
+  // and trails it at 90-98% -- both are bound near 5 TB/s of gathered L2 rows
   const char* e = getenv("MCUBE_SPMM_PATH");
-  if (e && e[0] == 'm') return false;  // force the mma.sync path
+  if (!e || e[0] != 't') return false;
   const bool dense_items = p.batch == 1 || (p.rhs_stride * 4 == p.K * p.N && p.lhs_stride * 4 == p.stored * 8);
   return p.LB == 8 && p.RB == 8 && p.V == 8 && (p.S == 16 || p.S % 32 == 0) && p.N % 16 == 0 && dense_items &&
          p.stored > 0 && (reinterpret_cast<uintptr_t>(p.rhs_words) & 15) == 0 &&
@@ -405,12 +443,26 @@ cudaError_t launch_spmm_tc(SpmmParams p, cudaStream_t stream) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int per_sm = 4;
+  // ring depth x CTAs per SM = k-steps in flight per SM (tunable for experiments)
+  const char* es = getenv("MCUBE_SPMM_STAGES");
+  const char* ec = getenv("MCUBE_SPMM_CTAS");
+  const int stages = es ? atoi(es) : 16;
+  const char* eg = getenv("MCUBE_SPMM_GATHER");
+  p.gather_tma = (eg && eg[0] == 't') ? 1 : 0;
+  const int per_sm = ec ? atoi(ec) : 2;
   const long long want = static_cast<long long>(sms) * per_sm;
   const int grid = static_cast<int>(p.tasks < want ? p.tasks : want);
   if (grid == 0) return cudaSuccess;
-  cudaFuncSetAttribute(spmm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemL::TOTAL);
-  spmm_tc_kernel<<<grid, kThreads, SmemL::TOTAL, stream>>>(tb, tl, p);
+  if (stages >= 16) {
+    cudaFuncSetAttribute(spmm_tc_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemL<16>::TOTAL);
+    spmm_tc_kernel<16><<<grid, kThreads, SmemL<16>::TOTAL, stream>>>(tb, tl, p);
+  } else if (stages >= 12) {
+    cudaFuncSetAttribute(spmm_tc_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemL<12>::TOTAL);
+    spmm_tc_kernel<12><<<grid, kThreads, SmemL<12>::TOTAL, stream>>>(tb, tl, p);
+  } else {
+    cudaFuncSetAttribute(spmm_tc_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemL<8>::TOTAL);
+    spmm_tc_kernel<8><<<grid, kThreads, SmemL<8>::TOTAL, stream>>>(tb, tl, p);
+  }
   count_launch();
   return cudaGetLastError();
 }

@@ -385,8 +385,11 @@ def test_spmm_l8r8_paths_vs_oracle(path, shape, monkeypatch):
     assert (np.asarray(out) == want).all()
 
 
+@pytest.mark.parametrize("gather", ["cpasync", "tma"])
 @pytest.mark.parametrize("stride", [16, 32])
-def test_spmm_tc_irregular_rows(stride):
+def test_spmm_tc_irregular_rows(stride, gather, monkeypatch):
+    monkeypatch.setenv("MCUBE_SPMM_PATH", "tc")
+    monkeypatch.setenv("MCUBE_SPMM_GATHER", "tma" if gather == "tma" else "cp")
     m, n, k = 640, 256, 1536
     begin, end, sidx, svals = _spmm_irregular(m, k, 8, 5 + stride, stride)
     rng = np.random.default_rng(9)
