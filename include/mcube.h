@@ -106,6 +106,16 @@ typedef struct mc_epilogue {
 int mc_spmm(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n,
             int32_t* out, uint32_t* status, void* stream);
 
+/* SpMM with a caller-provided device workspace (same contract as mc_spmm otherwise).
+ * At moderate sparsity (stored*V >= 8% of M*K, M/N/K multiples of 128) the library
+ * densifies the LHS into int8 chunk planes inside the workspace and runs an exact
+ * tcgen05 GEMM; results are bit-identical to the gather path. mc_spmm_workspace
+ * returns the bytes that path needs (0: the problem always runs on the gather
+ * kernels and the workspace may be NULL). Replaces kernels.spmm (kernels.py:293-298). */
+int mc_spmm_workspace(const mc_srbcrs* lhs, const mc_dense* rhs, size_t* bytes);
+int mc_spmm_ws(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n,
+               int32_t* out, uint32_t* status, void* workspace,
+               size_t workspace_bytes, void* stream);
 /* Batched SpMM over `batch` problems sharing the SR-BCRS structure
  * (row offsets and column indices) -- e.g. the attention heads of
  * attention.py:190-197. Item b uses lhs->words + b*lhs_words_stride,

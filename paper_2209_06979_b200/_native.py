@@ -72,6 +72,10 @@ class McAttentionArgs(ctypes.Structure):
 # entry point -> (restype, argtypes)
 _SIGNATURES = {
     "mc_spmm": (_i32, [ctypes.POINTER(McSrBcrs), ctypes.POINTER(McDense), _i32, _p, _p, _p]),
+    "mc_spmm_workspace": (_i32, [ctypes.POINTER(McSrBcrs), ctypes.POINTER(McDense),
+                                 ctypes.POINTER(ctypes.c_size_t)]),
+    "mc_spmm_ws": (_i32, [ctypes.POINTER(McSrBcrs), ctypes.POINTER(McDense), _i32, _p, _p, _p,
+                          ctypes.c_size_t, _p]),
     "mc_spmm_batched": (_i32, [ctypes.POINTER(McSrBcrs), _i64, ctypes.POINTER(McDense), _i64, _i32,
                                ctypes.POINTER(McEpilogue), _p, _i64, _p, _p]),
     "mc_sddmm": (_i32, [ctypes.POINTER(McDense), ctypes.POINTER(McDense), ctypes.POINTER(McBcrs),

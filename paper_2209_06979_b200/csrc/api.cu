@@ -121,12 +121,9 @@ int64_t mc_launch_count(int32_t reset) {
   return n;
 }
 
-int mc_spmm_batched(const mc_srbcrs* lhs, int64_t lhs_words_stride, const mc_dense* rhs, int64_t rhs_words_stride,
-                    int32_t batch, const mc_epilogue* epi, int32_t* out, int64_t out_stride, uint32_t* status,
-                    void* stream) {
-  int rc = check_spmm(lhs, rhs, 64);
-  if (rc) return rc;
-  if (batch < 0) return fail(MC_ERR_VALUE, "batch must be >= 0");
+static SpmmParams spmm_params(const mc_srbcrs* lhs, int64_t lhs_words_stride, const mc_dense* rhs,
+                               int64_t rhs_words_stride, int32_t batch, const mc_epilogue* epi, int32_t* out,
+                               int64_t out_stride, uint32_t* status) {
   SpmmParams p{};
   p.M = lhs->scalar_rows;
   p.K = lhs->scalar_cols;
@@ -155,6 +152,16 @@ int mc_spmm_batched(const mc_srbcrs* lhs, int64_t lhs_words_stride, const mc_den
     p.f16_stride = epi->out_f16_batch_stride;
   }
   p.status = status;
+  return p;
+}
+
+int mc_spmm_batched(const mc_srbcrs* lhs, int64_t lhs_words_stride, const mc_dense* rhs, int64_t rhs_words_stride,
+                    int32_t batch, const mc_epilogue* epi, int32_t* out, int64_t out_stride, uint32_t* status,
+                    void* stream) {
+  int rc = check_spmm(lhs, rhs, 64);
+  if (rc) return rc;
+  if (batch < 0) return fail(MC_ERR_VALUE, "batch must be >= 0");
+  SpmmParams p = spmm_params(lhs, lhs_words_stride, rhs, rhs_words_stride, batch, epi, out, out_stride, status);
   if (p.M == 0 || p.N == 0 || batch == 0) return MC_OK;
   return cuda_status(launch_spmm(p, static_cast<cudaStream_t>(stream)), "mc_spmm");
 }
@@ -163,6 +170,29 @@ int mc_spmm(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n, int32_t* ou
   int rc = check_spmm(lhs, rhs, bs_n);
   if (rc) return rc;
   return mc_spmm_batched(lhs, 0, rhs, 0, 1, nullptr, out, 0, status, stream);
+}
+
+int mc_spmm_workspace(const mc_srbcrs* lhs, const mc_dense* rhs, size_t* bytes) {
+  int rc = check_spmm(lhs, rhs, 64);
+  if (rc) return rc;
+  if (!bytes) return fail(MC_ERR_VALUE, "bytes must not be NULL");
+  // a placeholder output pointer: eligibility only looks at its alignment
+  SpmmParams p = spmm_params(lhs, 0, rhs, 0, 1, nullptr, reinterpret_cast<int32_t*>(256), 0, nullptr);
+  *bytes = dense_spmm_workspace(p);
+  return MC_OK;
+}
+
+int mc_spmm_ws(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n, int32_t* out, uint32_t* status,
+               void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = check_spmm(lhs, rhs, bs_n);
+  if (rc) return rc;
+  SpmmParams p = spmm_params(lhs, 0, rhs, 0, 1, nullptr, out, 0, status);
+  if (p.M == 0 || p.N == 0) return MC_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t need = dense_spmm_workspace(p);
+  if (workspace && need > 0 && workspace_bytes >= need)
+    return cuda_status(launch_dense_spmm(p, workspace, s), "mc_spmm_ws");
+  return cuda_status(launch_spmm(p, s), "mc_spmm_ws");
 }
 
 int mc_sddmm_batched(const mc_dense* a, int64_t a_words_stride, const mc_dense* b, int64_t b_words_stride,

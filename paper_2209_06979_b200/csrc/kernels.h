@@ -71,6 +71,13 @@ struct SddmmTcParams {
 };
 
 cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream);
+// dense-tile path for moderate sparsity (dense.cu + gemm_tc.cu): densify the LHS into int8
+// planes in a caller-provided workspace, then an exact tcgen05 GEMM
+bool dense_spmm_eligible(const SpmmParams& p);
+size_t dense_spmm_workspace(const SpmmParams& p);
+cudaError_t launch_dense_spmm(SpmmParams p, void* workspace, cudaStream_t stream);
+cudaError_t launch_gemm_tc(const SpmmParams& p, const int8_t* a0, const int8_t* a1, const int8_t* b0,
+                           const int8_t* b1, cudaStream_t stream);
 // tcgen05 gather path (spmm_tc.cu); launch_spmm dispatches to it when supported
 bool spmm_tc_supported(const SpmmParams& p);
 cudaError_t launch_spmm_tc(SpmmParams p, cudaStream_t stream);

@@ -127,7 +127,13 @@ def spmm_device(p: SpmmProblem, out=None, stream=None, check_status: bool = True
         out = t.empty((p.lhs.scalar_rows, p.rhs.cols), dtype=t.int32, device="cuda")
     status = D.status_word()
     s = N.stream_ptr(stream)
-    N.check(lib.mc_spmm(lhs, rhs, p.config.bs_n, N.ptr(out), N.ptr(status), s))
+    # moderate sparsity: the library densifies the LHS into a workspace and runs an exact
+    # tcgen05 GEMM (mc_spmm_workspace reports 0 when the gather kernels are used)
+    need = N.ctypes.c_size_t(0)
+    N.check(lib.mc_spmm_workspace(lhs, rhs, N.ctypes.byref(need)))
+    ws = t.empty(int(need.value), dtype=t.uint8, device=out.device) if need.value else None
+    N.check(lib.mc_spmm_ws(lhs, rhs, p.config.bs_n, N.ptr(out), N.ptr(status), N.ptr(ws),
+                           int(need.value), s))
     if check_status:
         D.fetch_status(status, stream)
     return out

@@ -398,3 +398,41 @@ def test_spmm_tc_irregular_rows(stride, gather, monkeypatch):
     out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(rhs, 8)))
     want = O.spmm(begin, end, sidx, svals, 8, stride, False, 8, rhs, 8, n)
     assert (np.asarray(out) == want).all()
+
+
+# ---------------- dense-tile SpMM (densify + exact tcgen05 GEMM) vs the oracle ----------------
+
+@pytest.mark.parametrize("pair", PAIRS)
+@pytest.mark.parametrize("v", [2, 4, 8])
+@pytest.mark.parametrize("sparsity", [0.5, 0.9, 0.98])
+def test_spmm_dense_path_vs_oracle(pair, v, sparsity, monkeypatch):
+    lb, rb = pair
+    monkeypatch.setenv("MCUBE_SPMM_PATH", "dense")
+    m, n, k = 256, 256, 512
+    c = O.build_spmm_case(m, n, k, v, sparsity, lb, rb, seed=lb * 100 + rb + v + int(sparsity * 100))
+    lhs = mc.SrBcrsMatrix(m, k, v, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                          mc.PackedArray.from_values(c["values"], lb), shuffled=c["shuffled"])
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], rb)))
+    want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], v, c["stride"],
+                  c["shuffled"], lb, c["rhs"], rb, n)
+    assert (np.asarray(out) == want).all()
+
+
+def test_spmm_dense_path_irregular_and_c3_rows(monkeypatch):
+    """Irregular rows (empty / full / clustered) and a C3-size L8-R8 problem on the dense path."""
+    monkeypatch.setenv("MCUBE_SPMM_PATH", "dense")
+    m, n, k = 640, 256, 1536
+    begin, end, sidx, svals = _spmm_irregular(m, k, 8, 77, 16)
+    rhs = np.random.default_rng(4).integers(-127, 128, size=(k, n))
+    lhs = mc.SrBcrsMatrix(m, k, 8, 16, begin, end, sidx, mc.PackedArray.from_values(svals, 8))
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(rhs, 8)))
+    assert (np.asarray(out) == O.spmm(begin, end, sidx, svals, 8, 16, False, 8, rhs, 8, n)).all()
+    c = O.build_spmm_case(4096, 512, 4096, 8, 0.9, 8, 8, seed=3)
+    lhs = mc.SrBcrsMatrix(4096, 4096, 8, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                          mc.PackedArray.from_values(c["values"], 8))
+    out = np.asarray(mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], 8))))
+    rows = list(range(0, 512, 41)) + [511]
+    want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], 8, c["stride"], False,
+                  8, c["rhs"], 8, 4096, rows=rows)
+    got = np.concatenate([out[r * 8:(r + 1) * 8] for r in rows])
+    assert (got == want).all()
