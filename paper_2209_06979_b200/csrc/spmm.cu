@@ -23,6 +23,8 @@
 // MMA fragments. Column indices for the next issue are prefetched one step ahead.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -32,13 +34,17 @@ namespace {
 
 constexpr int kWarps = 4;
 constexpr int kStages = 4;
-constexpr int kTileN = 64;
+constexpr int kSubN = 64;  // dense columns per MMA sub-tile (4 x m16 tiles)
 
-template <int LB, int RB, int V>
+// A warp task covers NS sub-tiles of 64 columns: NS > 1 widens each gathered row
+// segment to 128 bytes (one L2 line) for 4- and 8-bit RHS at large N.
+template <int LB, int RB, int V, int NS>
 struct SpmmCfg {
   static constexpr int LC = (LB >= 12) ? 2 : 1;        // LHS int8 chunks
   static constexpr int RC = (RB == 16) ? 2 : 1;        // RHS int8 chunks
-  static constexpr int RBYTES = kTileN * RB / 8;       // bytes of one gathered row segment
+  static constexpr int TN = kSubN * NS;                // dense columns per task
+  static constexpr int SUB = kSubN * RB / 8;           // bytes of one 64-column sub-segment
+  static constexpr int RBYTES = TN * RB / 8;           // bytes of one gathered row segment
   static constexpr int CPR = RBYTES / 16;              // 16-byte copies per row segment
   static constexpr int ABYTES = 2 * LB;                // bytes of 16 LHS values
   static constexpr int B_STAGE = 32 * RBYTES;
@@ -65,10 +71,10 @@ __device__ __forceinline__ int64_t idx_pos(int64_t q, bool shuffled) {
   return (q & ~7LL) | ((w >> 1) | ((w & 1) << 2));
 }
 
-template <int LB, int RB, int V, bool ALIGNED>
+template <int LB, int RB, int V, int NS, bool ALIGNED>
 __global__ void __launch_bounds__(kWarps * 32)
 spmm_kernel(const SpmmParams p) {
-  using C = SpmmCfg<LB, RB, V>;
+  using C = SpmmCfg<LB, RB, V, NS>;
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -79,7 +85,7 @@ spmm_kernel(const SpmmParams p) {
   const int64_t b = task / per_batch;
   const int64_t rem = task - b * per_batch;
   const int64_t r = rem / p.ntiles;
-  const int64_t c0 = (rem - r * p.ntiles) * kTileN;
+  const int64_t c0 = (rem - r * p.ntiles) * C::TN;
 
   const uint32_t* __restrict__ lhs = p.lhs_words + b * p.lhs_stride;
   const uint32_t* __restrict__ rhs = p.rhs_words + b * p.rhs_stride;
@@ -114,21 +120,13 @@ spmm_kernel(const SpmmParams p) {
   const uint64_t c0_bytes = static_cast<uint64_t>(c0) * RB / 8;
   const uint8_t* rhs_b = reinterpret_cast<const uint8_t*>(rhs);
   const uint32_t kdim = static_cast<uint32_t>(p.K);
-  uint32_t dst_off[C::CPR];
-  int kk_l[C::CPR], kk_p[C::CPR];
-  uint32_t colofs[C::CPR];
-  bool chunk_ok[C::CPR];
-#pragma unroll
-  for (int u = 0; u < C::CPR; ++u) {
-    const int q = lane + 32 * u;
-    const int kk = q / C::CPR, ch = q % C::CPR;
-    const int slot = slot_of(kk);
-    dst_off[u] = slot * C::RBYTES + ((ch * 16) ^ swz<C::RBYTES>(slot & 3));
-    kk_l[u] = kk;
-    kk_p[u] = shuffled ? ((kk & ~7) | (((kk & 7) >> 1) | ((kk & 1) << 2))) : kk;  // P^-1 within 8-groups
-    colofs[u] = static_cast<uint32_t>(c0_bytes) + ch * 16;
-    chunk_ok[u] = c0_bytes + ch * 16 < row_bytes;
-  }
+  // copy u of this lane moves 16-byte chunk ch of gathered row kk (CPR chunks per row);
+  // computed on demand (a hoisted array per copy costs 5 registers per chunk at CPR = 8)
+  auto kk_of = [&](int u) { return (lane + 32 * u) / C::CPR; };
+  auto ch_of = [&](int u) { return (lane + 32 * u) % C::CPR; };
+  auto kkp_of = [&](int kk) {  // P^-1 within 8-groups
+    return shuffled ? ((kk & ~7) | (((kk & 7) >> 1) | ((kk & 1) << 2))) : kk;
+  };
   // LHS value copies: lane -> (half h, row v, 8-byte part), constant per lane
   constexpr int kAPer = C::ABYTES / 8;
   constexpr int kACopies = (C::A_COPIES + 31) / 32;
@@ -141,7 +139,7 @@ spmm_kernel(const SpmmParams p) {
     const int base = ((step >> 3) & 1) * 256 + 32 * (step & 7);
 #pragma unroll
     for (int u = 0; u < C::CPR; ++u)
-      nidx[u] = (32 * step + kk_l[u] < stored32) ? sidx[base + kk_p[u]] : kSentinel;
+      nidx[u] = (32 * step + kk_of(u) < stored32) ? sidx[base + kkp_of(kk_of(u))] : kSentinel;
   };
 
   auto issue = [&](int step) {
@@ -152,13 +150,16 @@ spmm_kernel(const SpmmParams p) {
     const uint32_t sbase = wbuf_s + (step % kStages) * C::STAGE;
 #pragma unroll
     for (int u = 0; u < C::CPR; ++u) {
-      const uint32_t dst = sbase + dst_off[u];
+      const int slot = slot_of(kk_of(u));
+      const uint32_t dst = sbase + slot * C::RBYTES + ((ch_of(u) * 16) ^ swz<C::RBYTES>(slot & 3));
+      const uint32_t colofs = static_cast<uint32_t>(c0_bytes) + ch_of(u) * 16;
+      const bool chunk_ok = c0_bytes + ch_of(u) * 16 < row_bytes;
       const uint32_t col = nidx[u];
       bool ok = col < kdim;
       if (!ok && col != kSentinel) flag_status(p.status, MC_STATUS_BAD_INDEX);
       if constexpr (ALIGNED) {
-        const uint32_t nbytes = (ok && chunk_ok[u]) ? 16u : 0u;
-        const uint8_t* src = nbytes ? rhs_b + static_cast<uint64_t>(col) * row_bytes + colofs[u] : rhs_b;
+        const uint32_t nbytes = (ok && chunk_ok) ? 16u : 0u;
+        const uint8_t* src = nbytes ? rhs_b + static_cast<uint64_t>(col) * row_bytes + colofs : rhs_b;
         cp_async16(dst, src, nbytes);
       } else {
         const int ch = (lane + 32 * u) % C::CPR;
@@ -209,15 +210,17 @@ spmm_kernel(const SpmmParams p) {
     }
   };
 
-  int acc[C::LC][C::RC][4][4];
+  int acc[NS][C::LC][C::RC][4][4];
 #pragma unroll
-  for (int c = 0; c < C::LC; ++c)
+  for (int st = 0; st < NS; ++st)
 #pragma unroll
-    for (int j = 0; j < C::RC; ++j)
+    for (int c = 0; c < C::LC; ++c)
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int j = 0; j < C::RC; ++j)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) acc[c][j][q][e] = 0;
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[st][c][j][q][e] = 0;
 
   if (nsteps > 0) {
     fetch_idx_chunk(0);
@@ -277,6 +280,9 @@ spmm_kernel(const SpmmParams p) {
       }
     }
 
+    // NS column sub-tiles share the LHS fragments of the step
+#pragma unroll
+    for (int st = 0; st < NS; ++st) {
     // ---- MMA A operand: gathered rows, transposed to k-major words per column ----
     uint32_t T[C::RC][2][8];
 #pragma unroll
@@ -285,7 +291,7 @@ spmm_kernel(const SpmmParams p) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int slot = 16 * h + 4 * i + t;
-        const uint8_t* rp = sb + slot * C::RBYTES + ((g * RB) ^ swz<C::RBYTES>(t));
+        const uint8_t* rp = sb + slot * C::RBYTES + ((st * C::SUB + g * RB) ^ swz<C::RBYTES>(t));
         if constexpr (RB == 8) {
           const uint2 w = *reinterpret_cast<const uint2*>(rp);
           raw[i][0] = w.x;
@@ -339,12 +345,13 @@ spmm_kernel(const SpmmParams p) {
         for (int c = 0; c < C::LC; ++c) {
           const bool au = (RB == 16) && (j == 0);
           const bool bu = (LB >= 12) && (c == 0);
-          if (au && bu) mma16832<true, true>(acc[c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
-          else if (au) mma16832<true, false>(acc[c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
-          else if (bu) mma16832<false, true>(acc[c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
-          else mma16832<false, false>(acc[c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
+          if (au && bu) mma16832<true, true>(acc[st][c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
+          else if (au) mma16832<true, false>(acc[st][c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
+          else if (bu) mma16832<false, true>(acc[st][c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
+          else mma16832<false, false>(acc[st][c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
         }
       }
+    }
     }
     __syncwarp();
   }
@@ -352,6 +359,12 @@ spmm_kernel(const SpmmParams p) {
 
   // ---- epilogue: exact shift-add recombination + the reference's int32 checks ----
   bool overflow = false;
+  double alpha = 0.0;
+  if (p.out_f16) alpha = p.alpha ? p.alpha[b] : p.alpha_host;
+  const float alpha_f = static_cast<float>(alpha);
+  const int64_t row0 = r * V;
+#pragma unroll
+  for (int st = 0; st < NS; ++st) {
   int32_t vals[4][4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -362,8 +375,8 @@ spmm_kernel(const SpmmParams p) {
       for (int j = 0; j < C::RC; ++j) {
         long long tj;
         if constexpr (C::LC == 2) {
-          const long long lo = acc[0][j][q][e];
-          const long long hi = 256LL * acc[1][j][q][e];
+          const long long lo = acc[st][0][j][q][e];
+          const long long hi = 256LL * acc[st][1][j][q][e];
           constexpr bool w8 = (RB != 4);
           if constexpr (w8) {
             if constexpr (V == 8) overflow |= !fits_i32(hi);
@@ -373,7 +386,7 @@ spmm_kernel(const SpmmParams p) {
           }
           tj = lo + hi;
         } else {
-          tj = acc[0][j][q][e];
+          tj = acc[st][0][j][q][e];
         }
         total += tj << (8 * j);
       }
@@ -381,12 +394,6 @@ spmm_kernel(const SpmmParams p) {
       vals[q][e] = static_cast<int32_t>(total);
     }
   }
-  if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
-
-  double alpha = 0.0;
-  if (p.out_f16) alpha = p.alpha ? p.alpha[b] : p.alpha_host;
-  const float alpha_f = static_cast<float>(alpha);
-  const int64_t row0 = r * V;
 #pragma unroll
   for (int vv = 0; vv < 2; ++vv) {
     const int v = 2 * t + vv;
@@ -397,7 +404,7 @@ spmm_kernel(const SpmmParams p) {
       rowv[2 * q] = vals[q][vv];
       rowv[2 * q + 1] = vals[q][2 + vv];
     }
-    const int64_t n0 = c0 + 8 * g;
+    const int64_t n0 = c0 + st * kSubN + 8 * g;
     const int64_t base = (row0 + v) * p.N + n0;
     if (p.out) {
       int32_t* o = p.out + b * p.out_stride + base;
@@ -417,22 +424,26 @@ spmm_kernel(const SpmmParams p) {
         if (n0 + x < p.N) o[x] = f16_dequant(rowv[x], alpha, alpha_f);
     }
   }
+  }  // st
+  if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
 }
 
-template <int LB, int RB, int V>
-cudaError_t launch_spmm_v(const SpmmParams& p, cudaStream_t stream) {
-  using C = SpmmCfg<LB, RB, V>;
+template <int LB, int RB, int V, int NS>
+cudaError_t launch_spmm_v(SpmmParams p, cudaStream_t stream) {
+  using C = SpmmCfg<LB, RB, V, NS>;
+  p.ntiles = (p.N + C::TN - 1) / C::TN;
+  p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.ntiles;
   const int smem = kWarps * kStages * C::STAGE + kWarps * 2048;  // + per-warp index ring
   const bool aligned = ((p.N * RB) % 128 == 0) && ((reinterpret_cast<uintptr_t>(p.rhs_words) & 15) == 0) &&
                        ((p.rhs_stride * 4) % 16 == 0);
   const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
   if (grid == 0) return cudaSuccess;
   if (aligned) {
-    auto k = spmm_kernel<LB, RB, V, true>;
+    auto k = spmm_kernel<LB, RB, V, NS, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k<<<grid, kWarps * 32, smem, stream>>>(p);
   } else {
-    auto k = spmm_kernel<LB, RB, V, false>;
+    auto k = spmm_kernel<LB, RB, V, NS, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k<<<grid, kWarps * 32, smem, stream>>>(p);
   }
@@ -440,12 +451,27 @@ cudaError_t launch_spmm_v(const SpmmParams& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// Task width: 128-byte row segments (NS = 4 for R4, 2 for R8) when the problem still has
+// enough warp tasks to fill the GPU (C5-sized), else 64 columns (C3-sized, more tasks).
+template <int LB, int RB, int V>
+cudaError_t launch_spmm_ns(const SpmmParams& p, cudaStream_t stream) {
+  constexpr int kWide = RB == 4 ? (LB >= 12 ? 2 : 4) : (RB == 8 ? 2 : 1);  // two LHS chunks: register budget
+  const char* e = getenv("MCUBE_SPMM_NS");
+  const int64_t wide_tasks = static_cast<int64_t>(p.batch) * p.vrows * ((p.N + kSubN * kWide - 1) / (kSubN * kWide));
+  bool wide = kWide > 1 && wide_tasks >= 148LL * 48;
+  if (e) wide = atoi(e) > 1;
+  if constexpr (kWide > 1 && V == 8) {
+    if (wide) return launch_spmm_v<LB, RB, V, kWide>(p, stream);
+  }
+  return launch_spmm_v<LB, RB, V, 1>(p, stream);
+}
+
 template <int LB, int RB>
 cudaError_t launch_spmm_lr(const SpmmParams& p, cudaStream_t stream) {
   switch (p.V) {
-    case 2: return launch_spmm_v<LB, RB, 2>(p, stream);
-    case 4: return launch_spmm_v<LB, RB, 4>(p, stream);
-    default: return launch_spmm_v<LB, RB, 8>(p, stream);
+    case 2: return launch_spmm_ns<LB, RB, 2>(p, stream);
+    case 4: return launch_spmm_ns<LB, RB, 4>(p, stream);
+    default: return launch_spmm_ns<LB, RB, 8>(p, stream);
   }
 }
 
@@ -453,8 +479,6 @@ cudaError_t launch_spmm_lr(const SpmmParams& p, cudaStream_t stream) {
 
 cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream) {
   if (spmm_tc_supported(p)) return launch_spmm_tc(p, stream);
-  p.ntiles = (p.N + kTileN - 1) / kTileN;
-  p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.ntiles;
   const int key = p.LB * 100 + p.RB;
   switch (key) {
     case 1616: return launch_spmm_lr<16, 16>(p, stream);
