@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/mcube.h"
 
 namespace mcube {
@@ -139,6 +141,14 @@ __device__ __forceinline__ bool fits_i32(long long x) {
   return x >= -2147483648LL && x <= 2147483647LL;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may start while
+// the previous kernel on the stream drains; pdl_wait() blocks until that kernel has
+// completed and its memory is visible, so it must precede the first read of any input a
+// previous kernel could have produced. pdl_launch_dependents() lets the next kernel be
+// scheduled early. Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
+
 __device__ __forceinline__ uint16_t f16_bits_rn(double x) {
   __half h = __double2half(x);
   return *reinterpret_cast<uint16_t*>(&h);
@@ -155,6 +165,23 @@ __device__ __forceinline__ uint16_t f16_dequant(int32_t acc, double alpha, float
   const uint16_t hi = __half_as_ushort(__float2half_rn(y * 1.00000047683715820f));
   if (lo == hi) return lo;
   return f16_bits_rn(static_cast<double>(acc) * alpha);
+}
+
+// Launch `kern` with the programmatic-stream-serialization attribute (see pdl_wait).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 }  // namespace mcube

@@ -32,6 +32,8 @@ __global__ void __launch_bounds__(256)
 densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restrict__ plane1) {
   constexpr int LC = LB >= 12 ? 2 : 1;
   extern __shared__ __align__(16) uint8_t sm[];  // [LC][V][kKC] planes + kVB staged value words
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();
   const int64_t r = blockIdx.x;
   const int64_t k0 = static_cast<int64_t>(blockIdx.y) * kKC;
   const int kc = static_cast<int>((p.K - k0 < kKC) ? p.K - k0 : kKC);
@@ -153,9 +155,9 @@ cudaError_t launch_densify_v(const SpmmParams& p, int8_t* a0, int8_t* a1, cudaSt
   auto k = densify_kernel<LB, V>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(static_cast<unsigned>(p.vrows), static_cast<unsigned>((p.K + kKC - 1) / kKC));
-  k<<<grid, 256, smem, s>>>(p, a0, a1);
+  const cudaError_t e = launch_pdl(k, grid, dim3(256), smem, s, p, a0, a1);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int LB>

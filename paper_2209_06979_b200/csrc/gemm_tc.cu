@@ -87,6 +87,8 @@ gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
     for (int j = 0; j < RC; ++j) tc::prefetch_tmap(&maps.b[j]);
   }
   if (warp == 1) tc::tmem_alloc<512>(smem_u32(tmem_holder));
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();  // the A planes are written by the densify kernel just before
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -244,9 +246,9 @@ cudaError_t launch_lr(const GemmMaps& maps, const SpmmParams& p, cudaStream_t st
   const int grid = tiles < sms ? tiles : sms;
   auto k = gemm_tc_kernel<LC, RC, TN_>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
-  k<<<grid, 192, C::TOTAL, stream>>>(maps, p);
+  const cudaError_t e = launch_pdl(k, dim3(grid), dim3(192), C::TOTAL, stream, maps, p);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace

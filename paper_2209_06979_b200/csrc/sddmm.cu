@@ -80,6 +80,8 @@ sddmm_kernel(const SddmmParams p) {
   constexpr int RC = (RB == 16) ? 2 : 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();  // inputs may come from the previous kernel on the stream
   const int64_t task = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   if (task >= p.tasks) return;
   const int64_t per_batch = p.vrows * p.splits;
@@ -204,10 +206,20 @@ cudaError_t launch_v(const SddmmParams& p, cudaStream_t s) {
                        ((p.a_stride * 4) % 16 == 0) && ((p.b_stride * 4) % 16 == 0);
   const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
   if (grid == 0) return cudaSuccess;
-  if (aligned) sddmm_kernel<LB, RB, V, true><<<grid, kWarps * 32, 0, s>>>(p);
-  else sddmm_kernel<LB, RB, V, false><<<grid, kWarps * 32, 0, s>>>(p);
+  // same shared-memory carveout as the dense tcgen05 kernel: alternating launches of the two
+  // (the C2 sweep) then need no L1/shared reconfiguration between kernels
+  static bool carve = false;
+  if (!carve) {
+    cudaFuncSetAttribute(sddmm_kernel<LB, RB, V, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(sddmm_kernel<LB, RB, V, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
+  const cudaError_t e = aligned ? launch_pdl(sddmm_kernel<LB, RB, V, true>, dim3(grid), dim3(kWarps * 32), 0, s, p)
+                                : launch_pdl(sddmm_kernel<LB, RB, V, false>, dim3(grid), dim3(kWarps * 32), 0, s, p);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int LB, int RB>

@@ -237,20 +237,6 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (ce < cs + 1) ce = cs + 1;
     return make_int2(cs, ce);
   };
-  long long lo = 0, b_lo = 0, b_hi = 0, spec_lo = -1, spec_hi = -1;
-  int len = 0, cur = 0, mtop = 0, landed = 0, lo511 = 0, lo63 = 0, depth = 2, c_first = 0;
-  int mtop_last = 0;  // chunk bound of all cp.async groups but the most recent one
-  long long b_r = -1;
-  uint32_t b_c00 = 0;
-  if (warp >= kFirstBuild && warp < kFirstCons && t0 < t1) {
-    const int64_t rem0 = t0 % tiles_per_item;
-    b_r = (rem0 / p.n_ctiles) * VR + rl;
-    b_c00 = static_cast<uint32_t>((rem0 % p.n_ctiles) * kCols);
-    if (b_r < p.vrows) {  // the first panel's row offsets: in flight across the setup barrier
-      b_lo = p.row_offsets[b_r];
-      b_hi = p.row_offsets[b_r + 1];
-    }
-  }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(full_bar(s), 1);
@@ -271,6 +257,24 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     tc::prefetch_tmap(&tmB);
   }
   if (warp == 1) tc::tmem_alloc<512>(smem_u32(tmem_holder));
+  // everything above touches only this CTA's resources and the kernel parameters; inputs
+  // written by a previous kernel are read only after pdl_wait
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();
+  long long lo = 0, b_lo = 0, b_hi = 0, spec_lo = -1, spec_hi = -1;
+  int len = 0, cur = 0, mtop = 0, landed = 0, lo511 = 0, lo63 = 0, depth = 2, c_first = 0;
+  int mtop_last = 0;  // chunk bound of all cp.async groups but the most recent one
+  long long b_r = -1;
+  uint32_t b_c00 = 0;
+  if (warp >= kFirstBuild && warp < kFirstCons && t0 < t1) {
+    const int64_t rem0 = t0 % tiles_per_item;
+    b_r = (rem0 / p.n_ctiles) * VR + rl;
+    b_c00 = static_cast<uint32_t>((rem0 % p.n_ctiles) * kCols);
+    if (b_r < p.vrows) {  // the first panel's row offsets: in flight across the setup barrier
+      b_lo = p.row_offsets[b_r];
+      b_hi = p.row_offsets[b_r + 1];
+    }
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -703,9 +707,9 @@ cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream) {
     default: kern = sddmm_tc_kernel<4>; smem = Lay<4>::TOTAL; break;
   }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  kern<<<grid, kThreads, smem, stream>>>(ta, tb, q);
+  const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), smem, stream, ta, tb, q);
   count_launch();
-  return cudaGetLastError();
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace mcube

@@ -79,6 +79,8 @@ spmm_kernel(const SpmmParams p) {
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();  // inputs may come from the previous kernel on the stream (e.g. the attention softmax)
   const int64_t task = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
   if (task >= p.tasks) return;
   const int64_t per_batch = p.vrows * p.ntiles;
@@ -441,11 +443,11 @@ cudaError_t launch_spmm_v(SpmmParams p, cudaStream_t stream) {
   if (aligned) {
     auto k = spmm_kernel<LB, RB, V, NS, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<<<grid, kWarps * 32, smem, stream>>>(p);
+    if (const cudaError_t e = launch_pdl(k, dim3(grid), dim3(kWarps * 32), smem, stream, p)) return e;
   } else {
     auto k = spmm_kernel<LB, RB, V, NS, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k<<<grid, kWarps * 32, smem, stream>>>(p);
+    if (const cudaError_t e = launch_pdl(k, dim3(grid), dim3(kWarps * 32), smem, stream, p)) return e;
   }
   count_launch();
   return cudaGetLastError();
@@ -458,7 +460,7 @@ cudaError_t launch_spmm_ns(const SpmmParams& p, cudaStream_t stream) {
   constexpr int kWide = RB == 4 ? (LB >= 12 ? 2 : 4) : (RB == 8 ? 2 : 1);  // two LHS chunks: register budget
   const char* e = getenv("MCUBE_SPMM_NS");
   const int64_t wide_tasks = static_cast<int64_t>(p.batch) * p.vrows * ((p.N + kSubN * kWide - 1) / (kSubN * kWide));
-  bool wide = kWide > 1 && wide_tasks >= 148LL * 48;
+  bool wide = kWide > 1 && p.N >= kSubN * kWide && wide_tasks >= 148LL * 48;
   if (e) wide = atoi(e) > 1;
   if constexpr (kWide > 1 && V == 8) {
     if (wide) return launch_spmm_v<LB, RB, V, kWide>(p, stream);
