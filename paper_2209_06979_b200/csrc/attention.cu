@@ -10,6 +10,8 @@
 // the softmax in float32.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -89,6 +91,22 @@ __device__ __forceinline__ double h2d(uint16_t h) {
   return static_cast<double>(__half2float(x));
 }
 
+// fp16(e / sum) and its requantised value clip(rint(p16 / (1/smax))) (attention.py:127,
+// :157-162), both exactly as the reference's float64 chain: the product e * (1/sum) is within
+// 2 ulp of the quotient, so it decides the fp16 rounding unless a 2^-45 perturbation crosses
+// an fp16 boundary (then the division is taken); p16 * smax is exact in fp32 and never lies
+// within rounding distance of a .5 tie, so rintf of it equals rint(p16 / (1/smax)).
+__device__ __forceinline__ void prob_requant(double e, double sum, double inv_sum, int smax, uint16_t& pf,
+                                             int32_t& qi) {
+  const double pr = e * inv_sum;
+  pf = f16_bits_rn(pr);
+  if (f16_bits_rn(pr * 0.9999999999999716) != f16_bits_rn(pr * 1.0000000000000284)) pf = f16_bits_rn(e / sum);
+  __half h;
+  *reinterpret_cast<uint16_t*>(&h) = pf;
+  int q = static_cast<int>(rintf(__half2float(h) * static_cast<float>(smax)));
+  qi = q > smax ? smax : (q < -smax ? -smax : q);
+}
+
 // one warp per (head, vector row); lane owns blocks j = lane, lane+32, ...
 template <bool FAST>
 __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int64_t nblk8, const int64_t* offs,
@@ -105,7 +123,6 @@ __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int6
   const uint16_t* sc = scores + b * nblk8 + lo * 8;
   uint8_t* sv8 = reinterpret_cast<uint8_t*>(sr_vals + b * sr_stride_words);
   uint16_t* sv16 = reinterpret_cast<uint16_t*>(sr_vals + b * sr_stride_words);
-  const double sm_scale = 1.0 / static_cast<double>(smax);
 
   double mx[8], sum[8];
 #pragma unroll
@@ -133,6 +150,9 @@ __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int6
   for (int v = 0; v < 8; ++v)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum[v] += __shfl_xor_sync(0xffffffffu, sum[v], o);
+  double inv_sum[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) inv_sum[v] = 1.0 / sum[v];
 
   for (int64_t j = lane; j < stored; j += 32) {
     const int64_t pos = sbeg + j;
@@ -145,10 +165,9 @@ __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int6
         double e;
         if constexpr (FAST) e = static_cast<double>(__expf(static_cast<float>(h2d(hs[v]) - mx[v])));
         else e = exp(h2d(hs[v]) - mx[v]);
-        const uint16_t pf = f16_bits_rn(e / sum[v]);
-        double qd = rint(h2d(pf) / sm_scale);  // attention.py:158
-        qd = fmin(fmax(qd, -static_cast<double>(smax)), static_cast<double>(smax));
-        const int32_t qi = static_cast<int32_t>(qd);
+        uint16_t pf;
+        int32_t qi;
+        prob_requant(e, sum[v], inv_sum[v], smax, pf, qi);  // attention.py:127, :158
         const int64_t el = s * 8 * S + static_cast<int64_t>(v) * S + jj;
         if (sbits == 8) sv8[el] = static_cast<uint8_t>(qi);
         else sv16[el] = static_cast<uint16_t>(qi);
@@ -255,6 +274,186 @@ __global__ void quant8_f16_kernel(const __half* q, const __half* k, const __half
       make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// Fused score SDDMM + softmax + requant for 8-bit Q/K and d = 64 (attention.py:147-162):
+// one warp per (head, vector row). The row's scores are computed with mma.sync (16 mask
+// blocks x 8 query rows per MMA, K rows gathered from L2, d split 16 bytes per thread)
+// and dequantised exactly like the SDDMM epilogue (f16_dequant); they stay in shared
+// memory (kCap blocks per warp; longer rows recompute their chunks in each pass) and go
+// through the same float64 max / exp-sum / prob / requant sequence as
+// softmax_requant_kernel, which writes the SR-BCRS probability values the SpMM consumes.
+// Saves the fp16 score round trip through HBM and the score kernel's K = 64 padding.
+template <bool FAST>
+__global__ void __launch_bounds__(128)
+score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict__ kw, int64_t head_words,
+                     const int64_t* __restrict__ offs, const uint32_t* __restrict__ cols, int64_t vrows,
+                     int64_t L, const double* __restrict__ alpha_s, const int64_t* __restrict__ sr_begin, int S,
+                     int smax, int sbits, uint32_t* sr_vals, int64_t sr_stride_words, int64_t batch,
+                     uint32_t* status) {
+  constexpr int kCap = 512;  // cached blocks per warp (8 KB of fp16 scores)
+  __shared__ __align__(16) uint16_t sc_all[4][kCap * 8];
+  __shared__ uint32_t ix_all[4][kCap];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * 4 + warp;
+  if (gw >= batch * vrows) return;
+  const int64_t b = gw / vrows, r = gw - b * vrows;
+  uint16_t* sc = sc_all[warp];
+  const int64_t lo = offs[r], nb = offs[r + 1] - lo;
+  const double alpha = alpha_s[b];
+  const float alpha_f = static_cast<float>(alpha);
+  // query rows r*8 .. r*8+7 (MMA N = 8): this thread's 16 bytes d = 16t .. 16t+15 of row g
+  const uint4 qv = __ldg(reinterpret_cast<const uint4*>(qw + b * head_words + (r * 8 + g) * 16) + t);
+  const uint32_t* kh = kw + b * head_words;
+
+  // scores of blocks [j0, j0 + jn) into sc[(j - j0) * 8 + v]: the chunk's column indices
+  // are staged in shared memory by one coalesced pass, then the K rows of 4 groups of 16
+  // blocks are loaded before their MMAs (8 independent 16-byte loads in flight per lane)
+  uint32_t* ix = ix_all[warp];
+  auto compute = [&](int64_t j0, int jn) {
+    for (int i = lane; i < jn; i += 32) {
+      uint32_t c = __ldg(cols + lo + j0 + i);
+      if (c >= static_cast<uint32_t>(L)) {
+        flag_status(status, MC_STATUS_BAD_INDEX);
+        c = 0;
+      }
+      ix[i] = c;
+    }
+    __syncwarp();
+    for (int grp0 = 0; grp0 < jn; grp0 += 64) {
+      uint4 ka[4], kb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m0 = grp0 + 16 * u + g, m1 = m0 + 8;
+        const uint32_t c_lo = m0 < jn ? ix[m0] : 0u;
+        const uint32_t c_hi = m1 < jn ? ix[m1] : 0u;
+        ka[u] = __ldg(reinterpret_cast<const uint4*>(kh + static_cast<int64_t>(c_lo) * 16) + t);
+        kb[u] = __ldg(reinterpret_cast<const uint4*>(kh + static_cast<int64_t>(c_hi) * 16) + t);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int m0 = grp0 + 16 * u + g, m1 = m0 + 8;
+        if (grp0 + 16 * u >= jn) break;
+        int acc[4] = {0, 0, 0, 0};
+        mma16832<false, false>(acc, ka[u].x, kb[u].x, ka[u].y, kb[u].y, qv.x, qv.y);  // d 16t + 0..7
+        mma16832<false, false>(acc, ka[u].z, kb[u].z, ka[u].w, kb[u].w, qv.z, qv.w);  // d 16t + 8..15
+        // c0 = S[block g][query 2t], c1 = [g][2t+1], c2 = [g+8][2t], c3 = [g+8][2t+1]
+        const uint32_t h01 = static_cast<uint32_t>(f16_dequant(acc[0], alpha, alpha_f)) |
+                             (static_cast<uint32_t>(f16_dequant(acc[1], alpha, alpha_f)) << 16);
+        const uint32_t h23 = static_cast<uint32_t>(f16_dequant(acc[2], alpha, alpha_f)) |
+                             (static_cast<uint32_t>(f16_dequant(acc[3], alpha, alpha_f)) << 16);
+        if (m0 < jn) reinterpret_cast<uint32_t*>(sc)[(m0 * 8 + 2 * t) >> 1] = h01;
+        if (m1 < jn) reinterpret_cast<uint32_t*>(sc)[(m1 * 8 + 2 * t) >> 1] = h23;
+      }
+    }
+    __syncwarp();
+  };
+  const bool cached = nb <= kCap;
+  if (cached) compute(0, static_cast<int>(nb));
+
+  // pass 1: row maxima (fp16 scores compare exactly in fp32)
+  float mxf[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) mxf[v] = -INFINITY;
+  for (int64_t j0 = 0; j0 < nb; j0 += kCap) {
+    const int jn = static_cast<int>(nb - j0 < kCap ? nb - j0 : kCap);
+    if (!cached) { __syncwarp(); compute(j0, jn); }
+    for (int j = lane; j < jn; j += 32) {
+      const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
+      const __half* hs = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) mxf[v] = fmaxf(mxf[v], __half2float(hs[v]));
+    }
+  }
+  double mx[8], sum[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mxf[v] = fmaxf(mxf[v], __shfl_xor_sync(0xffffffffu, mxf[v], o));
+    mx[v] = static_cast<double>(mxf[v]);
+    sum[v] = 0.0;
+  }
+  // pass 2: sum of exp(x - max) (attention.py:120-124). Parity: float64 exp; fast: fp32 exp
+  // (x - max is exact in fp32 for fp16 x) accumulated as an fp32 (hi, lo) TwoSum pair.
+  float shi[8], slo[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) shi[v] = slo[v] = 0.f;
+  for (int64_t j0 = 0; j0 < nb; j0 += kCap) {
+    const int jn = static_cast<int>(nb - j0 < kCap ? nb - j0 : kCap);
+    if (!cached) { __syncwarp(); compute(j0, jn); }
+    for (int j = lane; j < jn; j += 32) {
+      const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
+      const __half* hs = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        if constexpr (FAST) {
+          const float e = __expf(__half2float(hs[v]) - mxf[v]);
+          const float t1 = shi[v] + e;
+          const float bp = t1 - shi[v];
+          slo[v] += (shi[v] - (t1 - bp)) + (e - bp);
+          shi[v] = t1;
+        } else {
+          sum[v] += exp(static_cast<double>(__half2float(hs[v])) - mx[v]);
+        }
+      }
+    }
+  }
+  double inv_sum[8];
+  float thr[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    if constexpr (FAST) sum[v] = static_cast<double>(shi[v]) + static_cast<double>(slo[v]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum[v] += __shfl_xor_sync(0xffffffffu, sum[v], o);
+    inv_sum[v] = 1.0 / sum[v];
+    // requant level q >= 1 needs p16 * smax >= 0.5, i.e. p > 0.4998 / smax, i.e.
+    // x - max > ln(0.4998 * sum / smax); below the (10 % lower) threshold q is exactly 0
+    thr[v] = mxf[v] + static_cast<float>(log(0.45 * sum[v] / static_cast<double>(smax)));
+  }
+  // pass 3: requantised probabilities into the SR-BCRS values (:157-162); only the few
+  // elements above the threshold evaluate exp and the fp16 rounding chain
+  const int64_t sbeg = sr_begin[r];
+  const int64_t stored = ((nb + S - 1) / S) * S;
+  uint8_t* sv8 = reinterpret_cast<uint8_t*>(sr_vals + b * sr_stride_words);
+  uint16_t* sv16 = reinterpret_cast<uint16_t*>(sr_vals + b * sr_stride_words);
+  for (int64_t j0 = 0; j0 < stored; j0 += kCap) {
+    const int jn = static_cast<int>(nb - j0 < kCap ? (nb - j0 > 0 ? nb - j0 : 0) : kCap);
+    const int jst = static_cast<int>(stored - j0 < kCap ? stored - j0 : kCap);
+    if (!cached && jn > 0) { __syncwarp(); compute(j0, jn); }
+    for (int j = lane; j < jst; j += 32) {
+      const int64_t pos = sbeg + j0 + j;
+      const int64_t s_ = pos / S, jj = pos - s_ * S;
+      int32_t qv[8];
+      if (j < jn) {
+        const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
+        const __half* hs = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const float xf = __half2float(hs[v]);
+          qv[v] = 0;
+          if (xf >= thr[v]) {
+            double e;
+            if constexpr (FAST) e = static_cast<double>(__expf(xf - mxf[v]));
+            else e = exp(static_cast<double>(xf) - mx[v]);
+            uint16_t pf;
+            prob_requant(e, sum[v], inv_sum[v], smax, pf, qv[v]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < 8; ++v) qv[v] = 0;
+      }
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const int64_t el = s_ * 8 * S + static_cast<int64_t>(v) * S + jj;
+        if (sbits == 8) sv8[el] = static_cast<uint8_t>(qv[v]);
+        else sv16[el] = static_cast<uint16_t>(qv[v]);
+      }
+    }
+  }
+}
+
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 }  // namespace
@@ -349,6 +548,22 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
     spmm_idx = sr_idx2;
   }
 
+  const bool fused = qb == 8 && d == 64 && !a->scores_int && !a->scores_f16 && !a->probs_f16 && !a->probs_int &&
+                     !getenv("MCUBE_ATTN_UNFUSED");
+  if (fused) {
+    // score SDDMM + softmax + requant in one kernel (scores never leave the SM)
+    const unsigned fgrid = static_cast<unsigned>((B * vrows + 3) / 4);
+    const uint32_t* kq = qkv + B * qwords;
+    cudaError_t e2 = a->mode == MC_ATTN_FAST
+                         ? launch_pdl(score_softmax_kernel<true>, dim3(fgrid), dim3(128), 0, stream, qkv, kq, qwords,
+                                      a->mask->row_offsets, a->mask->col_indices, vrows, L, alpha_s, sr_begin, S, smax,
+                                      sb, sr_vals, sr_words, B, status)
+                         : launch_pdl(score_softmax_kernel<false>, dim3(fgrid), dim3(128), 0, stream, qkv, kq, qwords,
+                                      a->mask->row_offsets, a->mask->col_indices, vrows, L, alpha_s, sr_begin, S, smax,
+                                      sb, sr_vals, sr_words, B, status);
+    count_launch();
+    if (e2 != cudaSuccess) return e2;
+  } else {
   SddmmParams sp{};
   sp.M = L; sp.K = d; sp.N = L; sp.vrows = vrows; sp.n_blocks = nblk;
   sp.V = 8; sp.LB = qb; sp.RB = qb; sp.batch = static_cast<int>(B);
@@ -370,6 +585,7 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
     softmax_requant_kernel<false><<<grid, 256, 0, stream>>>(scores, nblk * 8, a->mask->row_offsets, vrows, sr_begin, S,
                                                             smax, sb, sr_vals, sr_words, a->probs_f16, a->probs_int, B);
   count_launch();
+  }
 
   SpmmParams mp{};
   mp.M = L; mp.K = L; mp.N = d; mp.vrows = vrows;

@@ -436,3 +436,30 @@ def test_spmm_dense_path_irregular_and_c3_rows(monkeypatch):
                   8, c["rhs"], 8, 4096, rows=rows)
     got = np.concatenate([out[r * 8:(r + 1) * 8] for r in rows])
     assert (got == want).all()
+
+
+# ---------------- fused score + softmax kernel (8-bit, d = 64) ----------------
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+@pytest.mark.parametrize("L,sparsity", [(512, 0.9), (1024, 0.5), (768, 0.98)])
+def test_attention_fused_matches_unfused_and_oracle(mode, L, sparsity, monkeypatch):
+    """The fused kernel (no stage outputs requested) equals the unfused pipeline bit for bit
+    and the oracle (parity: exact; fast: within FAST_MODE_TOLERANCE). L=1024 at 50 % has rows
+    longer than the kernel's 512-block cache (recompute path)."""
+    import torch
+    d, heads = 64, 3
+    a = O.build_attention_case(L, d, sparsity, seed=L + int(sparsity * 100))
+    offs, cols = a["offsets"], a["col_indices"]
+    mask = mc.BcrsMatrix(L, L, 8, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * 8), 8))
+    cfg = mc.AttentionConfig(L, 8, 8, mask, head_dim=d, num_heads=heads)
+    g = torch.Generator(device="cuda").manual_seed(L)
+    q, k, v = (torch.randn((heads, L, d), device="cuda", generator=g).half() for _ in range(3))
+    fused = mc.AttentionRunner(cfg, heads, mode=mode)(q, k, v, check=True).clone()
+    monkeypatch.setenv("MCUBE_ATTN_UNFUSED", "1")
+    unfused = mc.AttentionRunner(cfg, heads, mode=mode)(q, k, v, check=True).clone()
+    assert torch.equal(fused, unfused)
+    for h in range(heads):
+        qh, kh, vh = (x[h].double().cpu().numpy() for x in (q, k, v))
+        ref = O.attention(qh, kh, vh, offs, cols, L, d, 8, 8)
+        err = float(np.abs(fused[h].double().cpu().numpy() - ref["output"]).max())
+        assert err <= (0.0 if mode == "parity" else mc.attention.FAST_MODE_TOLERANCE), (h, err)
