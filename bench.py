@@ -224,11 +224,19 @@ def run_ours(args):
     from paper_2209_06979_b200 import _native as Nn
 
     rank, world, local = dist_info()
+    # one process per GPU; MCUBE_BENCH_BACKEND=gloo lets several ranks share one device
+    # (used to exercise the N > 1 code path on a single-GPU box)
+    backend = os.environ.get("MCUBE_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     lib = Nn.lib()
     stream = torch.cuda.current_stream()
     sp = Nn.stream_ptr(stream)

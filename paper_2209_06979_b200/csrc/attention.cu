@@ -573,7 +573,6 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
   sp.out = a->scores_int; sp.out_stride = nblk * 8;
   sp.alpha = alpha_s; sp.out_f16 = scores; sp.f16_stride = nblk * 8;
   sp.status = status;
-  sp.f16_fast = 0;  // fp16(acc * alpha) rounded from float64 in both modes (exact)
   if ((err = launch_sddmm(sp, stream)) != cudaSuccess) return err;
 
   const int64_t warps = B * vrows;

@@ -47,7 +47,6 @@ struct SddmmParams {
   uint16_t* out_f16;
   int64_t f16_stride;
   uint32_t* status;
-  int f16_fast;  // fp16 epilogue in float32 (attention fast mode) instead of float64
   int splits;  // warps per vector row, chosen by the launcher
   int64_t tasks;
 };
@@ -64,7 +63,6 @@ struct SddmmTcParams {
   uint16_t* out_f16;
   int64_t f16_stride;
   uint32_t* status;
-  int f16_fast;
   int n_panels, n_ctiles;
   int64_t tiles;
   int debug;

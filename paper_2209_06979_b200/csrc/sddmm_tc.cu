@@ -688,7 +688,6 @@ cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream) {
   q.alpha = p.alpha;
   q.alpha_host = p.alpha_host;
   q.out_f16 = p.out_f16;
-  q.f16_fast = p.f16_fast;
   q.f16_stride = p.f16_stride;
   q.status = p.status;
   q.n_panels = static_cast<int>((p.M + kVRows * p.V - 1) / (kVRows * p.V));
