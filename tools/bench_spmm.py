@@ -104,7 +104,7 @@ def main():
         seed = O.cell_seed(0, ((512, 256, 512), 8, 0.9, "L8-R8"))
         res.append(dict(cfg="C1", **cell(512, 256, 512, 8, 0.9, 8, 8, seed, flush)))
     if "c3l8" in args:  # the tcgen05 path's cells: L8-R8, V=8
-        for sp in (0.7, 0.9, 0.98):
+        for sp in (0.7, 0.9, 0.95, 0.98):
             seed = O.cell_seed(0, ((4096, 512, 4096), 8, sp, "L8-R8"))
             r = dict(cfg="C3", **cell(4096, 512, 4096, 8, sp, 8, 8, seed, flush))
             res.append(r)
