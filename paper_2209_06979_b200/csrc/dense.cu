@@ -59,7 +59,18 @@ densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restri
     // staged words start at word w0: the batch's first element sits stage_skew bytes in
     const int stage_skew = static_cast<int>(((bit0 + qb * V * LB) - (w0 << 5)) >> 3);
     __syncthreads();  // previous batch's scatter (and the zero fill) done
-    for (int64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) vals[w - w0] = __ldg(p.lhs_words + w);
+    // 16-byte cp.async, all in flight together (w0 is 4-word aligned: rows start on stride
+    // boundaries, pb * V * LB is a multiple of 128 bits); the tail chunk is zero-filled
+    {
+      const uint32_t vs = smem_u32(vals);
+      const int64_t nw = w1 - w0;
+      for (int64_t c = threadIdx.x; c * 4 < nw; c += blockDim.x) {
+        const int64_t left = nw - c * 4;
+        const uint32_t bytes = left >= 4 ? 16u : static_cast<uint32_t>(left) * 4u;
+        cp_async16(vs + static_cast<uint32_t>(c) * 16, p.lhs_words + w0 + c * 4, bytes);
+      }
+      cp_async_commit();
+    }
     // this thread's column indices of the batch, loaded together with the staged values
     constexpr int kQ = 8;
     uint32_t cols[kQ];
@@ -68,6 +79,7 @@ densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restri
       const int64_t q = qb + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
       cols[u] = q < qe ? __ldg(p.col_indices + pb + index_pos(q, shuffled)) : kSentinel;
     }
+    cp_async_wait<0>();
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kQ; ++u) {

@@ -54,7 +54,10 @@ struct GemmMaps {
   CUtensorMap b[2];
 };
 
-template <int LC, int RC, int TN_>
+// CL > 1: clusters of CL CTAs along M, one tile per CTA; each B box is fetched in CL
+// row slices, one per CTA, multicast to the whole cluster (B traffic / CL), and every
+// CTA's MMA completion is multicast to the empty barriers of all CTAs of the cluster.
+template <int LC, int RC, int TN_, int CL>
 __global__ void __launch_bounds__(192, 1)
 gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
   using C = GemmCfg<LC, RC, TN_>;
@@ -76,7 +79,7 @@ gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       tc::mbar_init(full_bar(s), 1);
-      tc::mbar_init(empty_bar(s), 1);
+      tc::mbar_init(empty_bar(s), CL);  // one MMA-commit arrival per CTA of the cluster
     }
     for (int a = 0; a < C::SETS; ++a) {
       tc::mbar_init(tfull_bar(a), 1);
@@ -91,15 +94,25 @@ gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
   pdl_wait();  // the A planes are written by the densify kernel just before
   tc::tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) tc::cluster_sync();  // peers' barriers initialised before any multicast
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  const uint32_t crank = CL > 1 ? tc::cluster_ctarank() : 0u;
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CL) - 1u);
+  // tile schedule: persistent over all tiles (CL = 1) or one tile per CTA, the CL CTAs
+  // of a cluster on consecutive M tiles of one N tile (CL > 1)
+  const int t_first = CL > 1 ? ((blockIdx.x / CL) % nt) + (((blockIdx.x / CL) / nt) * CL + crank) * nt
+                             : static_cast<int>(blockIdx.x);
+  const int t_step = CL > 1 ? tiles : static_cast<int>(gridDim.x);
 
   if (warp == 0) {
     if (lane == 0) {
       uint32_t g = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = t_first; t < tiles; t += t_step) {
         const int m0 = (t / nt) * kTM, n0 = (t % nt) * kTN;
-        const int kr = t % KB;  // rotated k start: tiles sharing an operand box read it at different times
+        // rotated k start (CL = 1): tiles sharing an operand box read it at different times;
+        // a cluster walks k in lockstep (its CTAs share every B box)
+        const int kr = CL > 1 ? 0 : t % KB;
         for (int kk = 0; kk < KB; ++kk, ++g) {
           const int kb = (kk + kr) % KB;
           const int s = g % C::STAGES;
@@ -111,8 +124,13 @@ gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
 #pragma unroll
           for (int j = 0; j < RC; ++j)
 #pragma unroll
-            for (int nb = 0; nb < C::NB; ++nb)
-              tc::tma_load_2d(st + (LC + j * C::NB + nb) * kBox, &maps.b[j], full_bar(s), n0 + 128 * nb, kb * kKB);
+            for (int nb = 0; nb < C::NB; ++nb) {
+              if constexpr (CL > 1)  // this CTA's 128/CL k-row slice of the box, to every CTA
+                tc::tma_load_2d_mc(st + (LC + j * C::NB + nb) * kBox + crank * (kBox / CL), &maps.b[j], full_bar(s),
+                                   n0 + 128 * nb, kb * kKB + static_cast<int>(crank) * (kKB / CL), kMask);
+              else
+                tc::tma_load_2d(st + (LC + j * C::NB + nb) * kBox, &maps.b[j], full_bar(s), n0 + 128 * nb, kb * kKB);
+            }
         }
       }
     }
@@ -120,7 +138,7 @@ gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
     if (lane == 0) {
       uint32_t g = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      for (int t = t_first; t < tiles; t += t_step, ++it) {
         const int set = it % C::SETS;
         tc::mbar_wait(tempty_bar(set), ((it / C::SETS) & 1) ^ 1);
         tc::tc_fence_after();
@@ -144,7 +162,8 @@ gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
               }
             }
           }
-          tc::mma_commit(empty_bar(s));
+          if constexpr (CL > 1) tc::mma_commit_mc(empty_bar(s), kMask);
+          else tc::mma_commit(empty_bar(s));
         }
         tc::mma_commit(tfull_bar(set));
       }
@@ -153,7 +172,7 @@ gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
     // epilogue: warp w reads TMEM lanes 32*(w%4).., i.e. output rows m0 + 32*(w%4) + lane
     const int q = warp & 3;
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    for (int t = t_first; t < tiles; t += t_step, ++it) {
       const int set = it % C::SETS;
       const int m0 = (t / nt) * kTM, n0 = (t % nt) * kTN;
       tc::mbar_wait(tfull_bar(set), (it / C::SETS) & 1);
@@ -201,6 +220,7 @@ gemm_tc_kernel(const __grid_constant__ GemmMaps maps, const SpmmParams p) {
   }
   tc::tc_fence_before();
   __syncthreads();
+  if constexpr (CL > 1) tc::cluster_sync();  // no CTA leaves while peers may still signal it
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc<512>(tmem);
@@ -224,12 +244,12 @@ EncodeFn encode_fn() {
 }
 
 // 2-D int8 map [rows x cols] row-major, box 128 x 128, 128-byte swizzle
-bool map128(CUtensorMap* m, const void* base, int64_t rows, int64_t cols) {
+bool map128(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows = 128) {
   EncodeFn fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols)};
-  cuuint32_t box[2] = {128, 128};
+  cuuint32_t box[2] = {128, static_cast<cuuint32_t>(box_rows)};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -237,16 +257,39 @@ bool map128(CUtensorMap* m, const void* base, int64_t rows, int64_t cols) {
 }
 
 template <int LC, int RC, int TN_>
-cudaError_t launch_lr(const GemmMaps& maps, const SpmmParams& p, cudaStream_t stream) {
+cudaError_t launch_lr(const GemmMaps& maps, const SpmmParams& p, cudaStream_t stream, bool cluster) {
   using C = GemmCfg<LC, RC, TN_>;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = static_cast<int>((p.M / kTM) * (p.N / C::TN));
-  const int grid = tiles < sms ? tiles : sms;
-  auto k = gemm_tc_kernel<LC, RC, TN_>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
-  const cudaError_t e = launch_pdl(k, dim3(grid), dim3(192), C::TOTAL, stream, maps, p);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::TOTAL;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cudaError_t e;
+  if (cluster) {
+    constexpr int kCL = 4;
+    auto k = gemm_tc_kernel<LC, RC, TN_, kCL>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = kCL;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(tiles);
+    cfg.numAttrs = 2;
+    e = cudaLaunchKernelEx(&cfg, k, maps, p);
+  } else {
+    auto k = gemm_tc_kernel<LC, RC, TN_, 1>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL);
+    cfg.gridDim = dim3(tiles < sms ? tiles : sms);
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k, maps, p);
+  }
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -272,17 +315,23 @@ cudaError_t launch_gemm_tc(const SpmmParams& p, const int8_t* a0, const int8_t* 
   GemmMaps maps;
   memset(&maps, 0, sizeof(maps));
   const int lc = p.LB >= 12 ? 2 : 1, rc = p.RB == 16 ? 2 : 1;
+  // opt-in (MCUBE_GEMM_CLUSTER=1): clusters of 4 along M sharing each B box by TMA multicast.
+  // Measured: no L2-traffic or time saving at C3 (L2 already merges near-simultaneous
+  // unicast reads of a box by <= 4 CTAs), so the default is the persistent unicast kernel.
+  const char* ec = getenv("MCUBE_GEMM_CLUSTER");
+  const bool cluster = (p.M / kTM) % 4 == 0 && ec && ec[0] == '1';
+  const int brows = cluster ? kKB / 4 : kKB;
   if (!map128(&maps.a[0], a0, p.M, p.K) || (lc == 2 && !map128(&maps.a[1], a1, p.M, p.K)) ||
-      !map128(&maps.b[0], b0, p.K, p.N) || (rc == 2 && !map128(&maps.b[1], b1, p.K, p.N)))
+      !map128(&maps.b[0], b0, p.K, p.N, brows) || (rc == 2 && !map128(&maps.b[1], b1, p.K, p.N, brows)))
     return cudaErrorInvalidValue;
   if (lc == 1 && rc == 1) {
     const char* e = getenv("MCUBE_GEMM_TN");
-    if (e && atoi(e) == 256 && p.N % 256 == 0) return launch_lr<1, 1, 256>(maps, p, stream);
-    return launch_lr<1, 1, 0>(maps, p, stream);
+    if (e && atoi(e) == 256 && p.N % 256 == 0) return launch_lr<1, 1, 256>(maps, p, stream, cluster);
+    return launch_lr<1, 1, 0>(maps, p, stream, cluster);
   }
-  if (lc == 2 && rc == 1) return launch_lr<2, 1, 0>(maps, p, stream);
-  if (lc == 1 && rc == 2) return launch_lr<1, 2, 0>(maps, p, stream);
-  return launch_lr<2, 2, 0>(maps, p, stream);
+  if (lc == 2 && rc == 1) return launch_lr<2, 1, 0>(maps, p, stream, cluster);
+  if (lc == 1 && rc == 2) return launch_lr<1, 2, 0>(maps, p, stream, cluster);
+  return launch_lr<2, 2, 0>(maps, p, stream, cluster);
 }
 
 }  // namespace mcube

@@ -418,9 +418,12 @@ def test_spmm_dense_path_vs_oracle(pair, v, sparsity, monkeypatch):
     assert (np.asarray(out) == want).all()
 
 
-def test_spmm_dense_path_irregular_and_c3_rows(monkeypatch):
-    """Irregular rows (empty / full / clustered) and a C3-size L8-R8 problem on the dense path."""
+@pytest.mark.parametrize("cluster", ["0", "1"])
+def test_spmm_dense_path_irregular_and_c3_rows(cluster, monkeypatch):
+    """Irregular rows (empty / full / clustered) and a C3-size L8-R8 problem on the dense path
+    (persistent GEMM and the 4-CTA multicast-cluster variant)."""
     monkeypatch.setenv("MCUBE_SPMM_PATH", "dense")
+    monkeypatch.setenv("MCUBE_GEMM_CLUSTER", cluster)
     m, n, k = 640, 256, 1536
     begin, end, sidx, svals = _spmm_irregular(m, k, 8, 77, 16)
     rhs = np.random.default_rng(4).integers(-127, 128, size=(k, n))
@@ -463,3 +466,18 @@ def test_attention_fused_matches_unfused_and_oracle(mode, L, sparsity, monkeypat
         ref = O.attention(qh, kh, vh, offs, cols, L, d, 8, 8)
         err = float(np.abs(fused[h].double().cpu().numpy() - ref["output"]).max())
         assert err <= (0.0 if mode == "parity" else mc.attention.FAST_MODE_TOLERANCE), (h, err)
+
+
+@pytest.mark.parametrize("pair", [(8, 8), (16, 8), (8, 4)])
+def test_spmm_dense_path_k_beyond_one_densify_chunk(pair, monkeypatch):
+    """K = 8448 > 4096: the densify kernel covers each vector row in several column chunks."""
+    lb, rb = pair
+    monkeypatch.setenv("MCUBE_SPMM_PATH", "dense")
+    m, n, k = 256, 128, 8448
+    c = O.build_spmm_case(m, n, k, 8, 0.8, lb, rb, seed=k + lb + rb)
+    lhs = mc.SrBcrsMatrix(m, k, 8, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                          mc.PackedArray.from_values(c["values"], lb), shuffled=c["shuffled"])
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], rb)))
+    want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], 8, c["stride"],
+                  c["shuffled"], lb, c["rhs"], rb, n)
+    assert (np.asarray(out) == want).all()
