@@ -260,6 +260,27 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   // everything above touches only this CTA's resources and the kernel parameters; inputs
   // written by a previous kernel are read only after pdl_wait
   if (threadIdx.x == 0) pdl_launch_dependents();
+  // Warm L2 with this CTA's first operand boxes and pattern rows while the previous kernel
+  // drains: L2 is the coherence point, so a prefetch issued before pdl_wait cannot make a
+  // later read observe stale data; it only hides the first HBM round trips.
+  if (t0 < t1) {
+    const TileCursor c(t0, p.n_panels, p.n_ctiles);
+    if (warp == 0 && lane == 0) {
+      for (int kb = 0; kb < KB; ++kb) {
+        tc::tma_prefetch_2d(&tmA, kb * KBLK, static_cast<int>(c.item * p.M + c.panel * PANEL));
+        tc::tma_prefetch_2d(&tmB, kb * KBLK, static_cast<int>(c.item * p.N + c.ct * kCols));
+      }
+    } else if (warp >= kFirstBuild && warp < kFirstCons && (lane & (kLanesPerRow - 1)) == 0) {
+      const long long r = c.panel * VR + rl;
+      if (r < p.vrows) {
+        tc::prefetch_l2(p.row_offsets + r);
+        const long long g = (r * p.n_blocks) / p.vrows +
+                            static_cast<long long>((static_cast<double>(c.ct * kCols) / p.N) *
+                                                   (static_cast<double>(p.n_blocks) / p.vrows));
+        tc::prefetch_l2(p.col_indices + (g < p.n_blocks ? g : 0));
+      }
+    }
+  }
   pdl_wait();
   long long lo = 0, b_lo = 0, b_hi = 0, spec_lo = -1, spec_hi = -1;
   int len = 0, cur = 0, mtop = 0, landed = 0, lo511 = 0, lo63 = 0, depth = 2, c_first = 0;
