@@ -107,6 +107,49 @@ __device__ __forceinline__ void prob_requant(double e, double sum, double inv_su
   qi = q > smax ? smax : (q < -smax ? -smax : q);
 }
 
+// FAST-mode exp(x - max) shared by every kernel of the fast pipeline: ex2 of the fma
+// x * log2(e) - max * log2(e) (flush-to-zero), with mneg = -(max * log2 e) per row.
+constexpr float kLog2e = 1.4426950408889634f;
+__device__ __forceinline__ float att_exp_fast(float x, float mneg) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(fmaf(x, kLog2e, mneg)));
+  return y;
+}
+
+// Requant level from float32 arithmetic (FAST pipeline): p32 = e * fp32(1/sum) is within
+// 2^-23 (relative) of the float64 quotient e / sum, so fp16 of p32 * (1 -+ 2^-21) brackets
+// fp16(e / sum); when both ends give the same level that level is exact (it is what
+// prob_requant returns). Otherwise -1: the caller takes prob_requant (rare: p within 2^-21 of
+// an fp16 tie whose two neighbours straddle a requant level).
+__device__ __forceinline__ int prob_q_fast(float e, float inv_f, float smax_f) {
+  const float p = e * inv_f;
+  const float2 f = __half22float2(__floats2half2_rn(p * 0.99999952316284180f, p * 1.00000047683715820f));
+  const float ql = rintf(f.x * smax_f), qh = rintf(f.y * smax_f);
+  return ql == qh ? static_cast<int>(ql) : -1;
+}
+
+// packed fp32 pairs (FADD2 / FFMA2 on sm_100a)
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(unsigned long long r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 // one warp per (head, vector row); lane owns blocks j = lane, lane+32, ...
 template <bool FAST>
 __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int64_t nblk8, const int64_t* offs,
@@ -137,12 +180,15 @@ __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int6
   for (int v = 0; v < 8; ++v)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx[v] = fmax(mx[v], __shfl_xor_sync(0xffffffffu, mx[v], o));
+  float mneg[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) mneg[v] = -static_cast<float>(mx[v]) * kLog2e;
   for (int64_t j = lane; j < nb; j += 32) {
     const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
     const uint16_t* hs = reinterpret_cast<const uint16_t*>(&u);
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
-      if constexpr (FAST) sum[v] += static_cast<double>(__expf(static_cast<float>(h2d(hs[v]) - mx[v])));
+      if constexpr (FAST) sum[v] += static_cast<double>(att_exp_fast(static_cast<float>(h2d(hs[v])), mneg[v]));
       else sum[v] += exp(h2d(hs[v]) - mx[v]);
     }
   }
@@ -163,7 +209,7 @@ __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int6
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         double e;
-        if constexpr (FAST) e = static_cast<double>(__expf(static_cast<float>(h2d(hs[v]) - mx[v])));
+        if constexpr (FAST) e = static_cast<double>(att_exp_fast(static_cast<float>(h2d(hs[v])), mneg[v]));
         else e = exp(h2d(hs[v]) - mx[v]);
         uint16_t pf;
         int32_t qi;
@@ -282,24 +328,41 @@ __global__ void quant8_f16_kernel(const __half* q, const __half* k, const __half
 // through the same float64 max / exp-sum / prob / requant sequence as
 // softmax_requant_kernel, which writes the SR-BCRS probability values the SpMM consumes.
 // Saves the fp16 score round trip through HBM and the score kernel's K = 64 padding.
-template <bool FAST>
+constexpr int kAttCap = 512;  // cached mask blocks per warp (8 KB of fp16 scores)
+// per-warp shared memory of the fused kernel: scores [kCap][8] fp16, column indices
+// [kCap], and with MIX the int8 probabilities [8][kCap] + a 2-slot ring of 32 V rows
+template <bool MIX>
+constexpr int att_warp_smem() {
+  return kAttCap * 16 + kAttCap * 4 + (MIX ? kAttCap * 8 + 2 * 32 * 64 : 0);
+}
+
+// MIX: also the P x V product (attention.py:164-176) -- the requantised probabilities stay
+// in shared memory as the MMA B operand, the V rows of each 32-block k-step are gathered
+// by cp.async in the slot order / XOR swizzle of spmm.cu and byte-transposed with PRMT,
+// and the output is dequantised to fp16 in the epilogue (one kernel per layer after
+// quantisation); otherwise pass 3 writes the SR-BCRS probabilities for the SpMM kernel.
+template <bool FAST, bool MIX>
 __global__ void __launch_bounds__(128)
 score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict__ kw, int64_t head_words,
                      const int64_t* __restrict__ offs, const uint32_t* __restrict__ cols, int64_t vrows,
                      int64_t L, const double* __restrict__ alpha_s, const int64_t* __restrict__ sr_begin, int S,
                      int smax, int sbits, uint32_t* sr_vals, int64_t sr_stride_words, int64_t batch,
-                     uint32_t* status) {
-  constexpr int kCap = 512;  // cached blocks per warp (8 KB of fp16 scores)
-  __shared__ __align__(16) uint16_t sc_all[4][kCap * 8];
-  __shared__ uint32_t ix_all[4][kCap];
+                     uint32_t* status, const uint32_t* __restrict__ vw, const double* __restrict__ alpha_m,
+                     uint16_t* __restrict__ out_f16) {
+  constexpr int kCap = kAttCap;
+  extern __shared__ __align__(16) uint8_t att_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* wsm = att_smem + warp * att_warp_smem<MIX>();
+  uint16_t* sc = reinterpret_cast<uint16_t*>(wsm);
+  uint32_t* ix = reinterpret_cast<uint32_t*>(wsm + kCap * 16);
+  int8_t* pm = reinterpret_cast<int8_t*>(wsm + kCap * 20);        // MIX: P[v][kCap]
+  uint8_t* vring = wsm + kCap * 28;                               // MIX: 2 x 32 V rows x 64 B
   const int g = lane >> 2, t = lane & 3;
   if (threadIdx.x == 0) pdl_launch_dependents();
   pdl_wait();
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * 4 + warp;
   if (gw >= batch * vrows) return;
   const int64_t b = gw / vrows, r = gw - b * vrows;
-  uint16_t* sc = sc_all[warp];
   const int64_t lo = offs[r], nb = offs[r + 1] - lo;
   const double alpha = alpha_s[b];
   const float alpha_f = static_cast<float>(alpha);
@@ -310,7 +373,6 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
   // scores of blocks [j0, j0 + jn) into sc[(j - j0) * 8 + v]: the chunk's column indices
   // are staged in shared memory by one coalesced pass, then the K rows of 4 groups of 16
   // blocks are loaded before their MMAs (8 independent 16-byte loads in flight per lane)
-  uint32_t* ix = ix_all[warp];
   auto compute = [&](int64_t j0, int jn) {
     for (int i = lane; i < jn; i += 32) {
       uint32_t c = __ldg(cols + lo + j0 + i);
@@ -352,64 +414,194 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
   const bool cached = nb <= kCap;
   if (cached) compute(0, static_cast<int>(nb));
 
-  // pass 1: row maxima (fp16 scores compare exactly in fp32)
-  float mxf[8];
+  // pass 1: row maxima (fp16 scores compare exactly; packed half2 max)
+  __half2 mx2[4];
 #pragma unroll
-  for (int v = 0; v < 8; ++v) mxf[v] = -INFINITY;
+  for (int p = 0; p < 4; ++p) mx2[p] = __float2half2_rn(-INFINITY);
   for (int64_t j0 = 0; j0 < nb; j0 += kCap) {
     const int jn = static_cast<int>(nb - j0 < kCap ? nb - j0 : kCap);
     if (!cached) { __syncwarp(); compute(j0, jn); }
     for (int j = lane; j < jn; j += 32) {
       const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
-      const __half* hs = reinterpret_cast<const __half*>(&u);
+      const __half2* hs = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
-      for (int v = 0; v < 8; ++v) mxf[v] = fmaxf(mxf[v], __half2float(hs[v]));
+      for (int p = 0; p < 4; ++p) mx2[p] = __hmax2(mx2[p], hs[p]);
     }
   }
+  float mxf[8], mneg[8];
   double mx[8], sum[8];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const float2 f = __half22float2(mx2[p]);
+    mxf[2 * p] = f.x;
+    mxf[2 * p + 1] = f.y;
+  }
 #pragma unroll
   for (int v = 0; v < 8; ++v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mxf[v] = fmaxf(mxf[v], __shfl_xor_sync(0xffffffffu, mxf[v], o));
     mx[v] = static_cast<double>(mxf[v]);
+    mneg[v] = -mxf[v] * kLog2e;
     sum[v] = 0.0;
   }
-  // pass 2: sum of exp(x - max) (attention.py:120-124). Parity: float64 exp; fast: fp32 exp
-  // (x - max is exact in fp32 for fp16 x) accumulated as an fp32 (hi, lo) TwoSum pair.
-  float shi[8], slo[8];
+  // pass 2: sum of exp(x - max) (attention.py:120-124). Parity: float64 exp; fast:
+  // att_exp_fast accumulated as fp32 (hi, lo) TwoSum pairs, two rows per FADD2.
+  unsigned long long shi[4], slo[4];
 #pragma unroll
-  for (int v = 0; v < 8; ++v) shi[v] = slo[v] = 0.f;
+  for (int p = 0; p < 4; ++p) shi[p] = slo[p] = 0ull;
   for (int64_t j0 = 0; j0 < nb; j0 += kCap) {
     const int jn = static_cast<int>(nb - j0 < kCap ? nb - j0 : kCap);
     if (!cached) { __syncwarp(); compute(j0, jn); }
     for (int j = lane; j < jn; j += 32) {
       const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
-      const __half* hs = reinterpret_cast<const __half*>(&u);
+      const __half2* hs = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
-      for (int v = 0; v < 8; ++v) {
+      for (int p = 0; p < 4; ++p) {
+        const float2 x = __half22float2(hs[p]);
         if constexpr (FAST) {
-          const float e = __expf(__half2float(hs[v]) - mxf[v]);
-          const float t1 = shi[v] + e;
-          const float bp = t1 - shi[v];
-          slo[v] += (shi[v] - (t1 - bp)) + (e - bp);
-          shi[v] = t1;
+          const unsigned long long e = f2_pack(att_exp_fast(x.x, mneg[2 * p]), att_exp_fast(x.y, mneg[2 * p + 1]));
+          const unsigned long long t1 = f2_add(shi[p], e);
+          const unsigned long long bp = f2_sub(t1, shi[p]);
+          const unsigned long long err = f2_add(f2_sub(shi[p], f2_sub(t1, bp)), f2_sub(e, bp));
+          slo[p] = f2_add(slo[p], err);
+          shi[p] = t1;
         } else {
-          sum[v] += exp(static_cast<double>(__half2float(hs[v])) - mx[v]);
+          sum[2 * p] += exp(static_cast<double>(x.x) - mx[2 * p]);
+          sum[2 * p + 1] += exp(static_cast<double>(x.y) - mx[2 * p + 1]);
         }
       }
     }
   }
   double inv_sum[8];
-  float thr[8];
+  float thr[8], inv_f[8];
+  const float smax_f = static_cast<float>(smax);
 #pragma unroll
   for (int v = 0; v < 8; ++v) {
-    if constexpr (FAST) sum[v] = static_cast<double>(shi[v]) + static_cast<double>(slo[v]);
+    if constexpr (FAST) {
+      const float2 h = f2_unpack(shi[v >> 1]), l = f2_unpack(slo[v >> 1]);
+      sum[v] = (v & 1) ? static_cast<double>(h.y) + static_cast<double>(l.y)
+                       : static_cast<double>(h.x) + static_cast<double>(l.x);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum[v] += __shfl_xor_sync(0xffffffffu, sum[v], o);
     inv_sum[v] = 1.0 / sum[v];
+    inv_f[v] = static_cast<float>(inv_sum[v]);
     // requant level q >= 1 needs p16 * smax >= 0.5, i.e. p > 0.4998 / smax, i.e.
     // x - max > ln(0.4998 * sum / smax); below the (10 % lower) threshold q is exactly 0
     thr[v] = mxf[v] + static_cast<float>(log(0.45 * sum[v] / static_cast<double>(smax)));
+  }
+  // requant level of score x in row v (attention.py:127, :157-162)
+  auto level = [&](float xf, int v) -> int32_t {
+    if constexpr (FAST) {
+      const float e = att_exp_fast(xf, mneg[v]);
+      int q = prob_q_fast(e, inv_f[v], smax_f);
+      if (q < 0) {
+        uint16_t pf;
+        prob_requant(static_cast<double>(e), sum[v], inv_sum[v], smax, pf, q);
+      }
+      return q;
+    } else {
+      int32_t q = 0;
+      if (xf >= thr[v]) {
+        uint16_t pf;
+        prob_requant(exp(static_cast<double>(xf) - mx[v]), sum[v], inv_sum[v], smax, pf, q);
+      }
+      return q;
+    }
+  };
+  if constexpr (MIX) {
+    // pass 3 + P x V: per chunk, the int8 probabilities go to pm[v][j]; then k-steps of
+    // 32 blocks: V rows col_j (64 B each) gathered into slot order, D^T[n, v] += V^T P^T
+    // (mma.sync m16n8k32: M = 16 head dims per MMA, 4 per k-step; N = 8 query rows)
+    const uint8_t* vb = reinterpret_cast<const uint8_t*>(vw + b * head_words);
+    const uint32_t vring_s = smem_u32(vring);
+    int acc[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[q][e] = 0;
+    for (int64_t j0 = 0; j0 < nb; j0 += kCap) {
+      const int jn = static_cast<int>(nb - j0 < kCap ? nb - j0 : kCap);
+      if (!cached) { __syncwarp(); compute(j0, jn); }
+      const int jpad = (jn + 31) & ~31;
+      for (int j = lane; j < jpad; j += 32) {
+        int32_t qv[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) qv[v] = 0;
+        if (j < jn) {
+          const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
+          const __half* hs = reinterpret_cast<const __half*>(&u);
+#pragma unroll
+          for (int v = 0; v < 8; ++v) qv[v] = level(__half2float(hs[v]), v);
+        }
+#pragma unroll
+        for (int v = 0; v < 8; ++v) pm[v * kCap + j] = static_cast<int8_t>(qv[v]);
+      }
+      __syncwarp();
+      // gather of k-step s into ring slot s & 1: copy u of this lane moves 16-byte chunk
+      // ch of gathered row kk (4 chunks per 64-byte row), slot order + XOR swizzle as spmm.cu
+      auto gather = [&](int s) {
+        const uint32_t base = vring_s + (s & 1) * 2048;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int qq = lane + 32 * u;
+          const int kk = qq >> 2, ch = qq & 3;
+          const int jj = 32 * s + kk;
+          const int slot = ((kk >> 4) << 4) | ((kk & 3) << 2) | ((kk >> 2) & 3);
+          const uint32_t dst = base + slot * 64 + ((ch * 16) ^ (32 * ((slot & 3) >> 1)));
+          const bool ok = jj < jn;
+          cp_async16(dst, ok ? vb + static_cast<int64_t>(ix[jj]) * 64 + ch * 16 : vb, ok ? 16u : 0u);
+        }
+        cp_async_commit();
+      };
+      const int nsteps = jpad >> 5;
+      gather(0);
+      for (int s_ = 0; s_ < nsteps; ++s_) {
+        if (s_ + 1 < nsteps) gather(s_ + 1);
+        if (s_ + 1 < nsteps) cp_async_wait<1>();
+        else cp_async_wait<0>();
+        __syncwarp();
+        const uint8_t* sb = vring + (s_ & 1) * 2048;
+        // B operand: P[g][32 s + 16 h + 4 t .. +3]
+        uint32_t bf[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) bf[h] = *reinterpret_cast<const uint32_t*>(pm + g * kCap + 32 * s_ + 16 * h + 4 * t);
+        // A operand: gathered rows, transposed to k-major words per head dim
+        uint32_t T[2][8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t raw[4][2];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int slot = 16 * h + 4 * i + t;
+            const uint2 w = *reinterpret_cast<const uint2*>(sb + slot * 64 + ((g * 8) ^ (32 * (t >> 1))));
+            raw[i][0] = w.x;
+            raw[i][1] = w.y;
+          }
+          transpose4x4(raw[0][0], raw[1][0], raw[2][0], raw[3][0], T[h][0], T[h][1], T[h][2], T[h][3]);
+          transpose4x4(raw[0][1], raw[1][1], raw[2][1], raw[3][1], T[h][4], T[h][5], T[h][6], T[h][7]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)  // m = g <-> dim 8g + 2q, m = g + 8 <-> dim 8g + 2q + 1
+          mma16832<false, false>(acc[q], T[0][2 * q], T[0][2 * q + 1], T[1][2 * q], T[1][2 * q + 1], bf[0], bf[1]);
+        __syncwarp();
+      }
+    }
+    // epilogue: fp16(mix * alpha_m) (attention.py:169-176); acc[q]: (dim 8g+2q, v 2t), (8g+2q, 2t+1),
+    // (8g+2q+1, 2t), (8g+2q+1, 2t+1)
+    const double am = alpha_m[b];
+    const float am_f = static_cast<float>(am);
+#pragma unroll
+    for (int vv = 0; vv < 2; ++vv) {
+      const int v = 2 * t + vv;
+      uint32_t h4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        h4[q] = static_cast<uint32_t>(f16_dequant(acc[q][vv], am, am_f)) |
+                (static_cast<uint32_t>(f16_dequant(acc[q][2 + vv], am, am_f)) << 16);
+      *reinterpret_cast<uint4*>(out_f16 + (b * L + r * 8 + v) * 64 + 8 * g) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+    }
+    return;
   }
   // pass 3: requantised probabilities into the SR-BCRS values (:157-162); only the few
   // elements above the threshold evaluate exp and the fp16 rounding chain
@@ -429,17 +621,7 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
         const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
         const __half* hs = reinterpret_cast<const __half*>(&u);
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const float xf = __half2float(hs[v]);
-          qv[v] = 0;
-          if (xf >= thr[v]) {
-            double e;
-            if constexpr (FAST) e = static_cast<double>(__expf(xf - mxf[v]));
-            else e = exp(static_cast<double>(xf) - mx[v]);
-            uint16_t pf;
-            prob_requant(e, sum[v], inv_sum[v], smax, pf, qv[v]);
-          }
-        }
+        for (int v = 0; v < 8; ++v) qv[v] = level(__half2float(hs[v]), v);
       } else {
 #pragma unroll
         for (int v = 0; v < 8; ++v) qv[v] = 0;
@@ -534,6 +716,25 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
     count_launch();
   }
 
+  const bool fused = qb == 8 && d == 64 && !a->scores_int && !a->scores_f16 && !a->probs_f16 && !a->probs_int &&
+                     !getenv("MCUBE_ATTN_UNFUSED");
+  // whole layer in the fused kernel (P x V included) unless the int32 mix is requested
+  const bool mix = fused && sb == 8 && !a->mix_int && a->out_f16 && !getenv("MCUBE_ATTN_NOMIX");
+  if (mix) {
+    const unsigned fgrid = static_cast<unsigned>((B * vrows + 3) / 4);
+    const uint32_t* kq = qkv + B * qwords;
+    const uint32_t* vq = qkv + 2 * B * qwords;
+    const int smem = 4 * att_warp_smem<true>();
+    auto kf = a->mode == MC_ATTN_FAST ? score_softmax_kernel<true, true> : score_softmax_kernel<false, true>;
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const cudaError_t e2 = launch_pdl(kf, dim3(fgrid), dim3(128), static_cast<size_t>(smem), stream, qkv, kq, qwords,
+                                      a->mask->row_offsets, a->mask->col_indices, vrows, L, alpha_s,
+                                      static_cast<const int64_t*>(nullptr), S, smax, sb, static_cast<uint32_t*>(nullptr),
+                                      sr_words, B, status, vq, static_cast<const double*>(alpha_m), a->out_f16);
+    count_launch();
+    return e2;
+  }
+
   // mask -> SR-BCRS structure of the probability matrix (stride = plan tile k)
   if ((err = launch_srbcrs_plan(a->mask->row_offsets, vrows, S, sr_begin, sr_end, sr_total, stream)) != cudaSuccess)
     return err;
@@ -548,19 +749,18 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
     spmm_idx = sr_idx2;
   }
 
-  const bool fused = qb == 8 && d == 64 && !a->scores_int && !a->scores_f16 && !a->probs_f16 && !a->probs_int &&
-                     !getenv("MCUBE_ATTN_UNFUSED");
   if (fused) {
     // score SDDMM + softmax + requant in one kernel (scores never leave the SM)
     const unsigned fgrid = static_cast<unsigned>((B * vrows + 3) / 4);
     const uint32_t* kq = qkv + B * qwords;
-    cudaError_t e2 = a->mode == MC_ATTN_FAST
-                         ? launch_pdl(score_softmax_kernel<true>, dim3(fgrid), dim3(128), 0, stream, qkv, kq, qwords,
-                                      a->mask->row_offsets, a->mask->col_indices, vrows, L, alpha_s, sr_begin, S, smax,
-                                      sb, sr_vals, sr_words, B, status)
-                         : launch_pdl(score_softmax_kernel<false>, dim3(fgrid), dim3(128), 0, stream, qkv, kq, qwords,
-                                      a->mask->row_offsets, a->mask->col_indices, vrows, L, alpha_s, sr_begin, S, smax,
-                                      sb, sr_vals, sr_words, B, status);
+    const int smem = 4 * att_warp_smem<false>();
+    auto kf = a->mode == MC_ATTN_FAST ? score_softmax_kernel<true, false> : score_softmax_kernel<false, false>;
+    cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e2 = launch_pdl(kf, dim3(fgrid), dim3(128), static_cast<size_t>(smem), stream, qkv, kq, qwords,
+                                a->mask->row_offsets, a->mask->col_indices, vrows, L, alpha_s,
+                                static_cast<const int64_t*>(sr_begin), S, smax, sb, sr_vals, sr_words, B, status,
+                                static_cast<const uint32_t*>(nullptr), static_cast<const double*>(nullptr),
+                                static_cast<uint16_t*>(nullptr));
     count_launch();
     if (e2 != cudaSuccess) return e2;
   } else {

@@ -161,9 +161,10 @@ __device__ __forceinline__ uint16_t f16_bits_rn(double x) {
 // product next to an fp16 rounding boundary, ~1e-3 of the cases) take float64.
 __device__ __forceinline__ uint16_t f16_dequant(int32_t acc, double alpha, float alpha_f) {
   const float y = static_cast<float>(acc) * alpha_f;
-  const uint16_t lo = __half_as_ushort(__float2half_rn(y * 0.99999952316284180f));
-  const uint16_t hi = __half_as_ushort(__float2half_rn(y * 1.00000047683715820f));
-  if (lo == hi) return lo;
+  // both roundings in one packed F2FP
+  const __half2 h = __floats2half2_rn(y * 0.99999952316284180f, y * 1.00000047683715820f);
+  const uint32_t hb = *reinterpret_cast<const uint32_t*>(&h);
+  if ((hb & 0xffffu) == (hb >> 16)) return static_cast<uint16_t>(hb);
   return f16_bits_rn(static_cast<double>(acc) * alpha);
 }
 

@@ -446,7 +446,8 @@ def test_spmm_dense_path_irregular_and_c3_rows(cluster, monkeypatch):
 @pytest.mark.parametrize("mode", ["parity", "fast"])
 @pytest.mark.parametrize("L,sparsity", [(512, 0.9), (1024, 0.5), (768, 0.98)])
 def test_attention_fused_matches_unfused_and_oracle(mode, L, sparsity, monkeypatch):
-    """The fused kernel (no stage outputs requested) equals the unfused pipeline bit for bit
+    """The fused kernel (no stage outputs requested; P x V folded in) equals the score/softmax-only
+    fused kernel + SpMM and the unfused pipeline bit for bit
     and the oracle (parity: exact; fast: within FAST_MODE_TOLERANCE). L=1024 at 50 % has rows
     longer than the kernel's 512-block cache (recompute path)."""
     import torch
@@ -458,6 +459,9 @@ def test_attention_fused_matches_unfused_and_oracle(mode, L, sparsity, monkeypat
     g = torch.Generator(device="cuda").manual_seed(L)
     q, k, v = (torch.randn((heads, L, d), device="cuda", generator=g).half() for _ in range(3))
     fused = mc.AttentionRunner(cfg, heads, mode=mode)(q, k, v, check=True).clone()
+    monkeypatch.setenv("MCUBE_ATTN_NOMIX", "1")  # fused scores/softmax + separate SpMM
+    nomix = mc.AttentionRunner(cfg, heads, mode=mode)(q, k, v, check=True).clone()
+    assert torch.equal(fused, nomix)
     monkeypatch.setenv("MCUBE_ATTN_UNFUSED", "1")
     unfused = mc.AttentionRunner(cfg, heads, mode=mode)(q, k, v, check=True).clone()
     assert torch.equal(fused, unfused)
