@@ -370,15 +370,33 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
   const uint4 qv = __ldg(reinterpret_cast<const uint4*>(qw + b * head_words + (r * 8 + g) * 16) + t);
   const uint32_t* kh = kw + b * head_words;
 
+  // dequantisation brackets: fp16 of acc * alpha_{lo,hi} (alpha * (1 -+ 2^-22) in fp32) brackets
+  // fp16(acc * alpha) (fp32 error <= 2^-23); equal ends are the exact f16_dequant result
+  const float alpha_lo = static_cast<float>(alpha * 0.99999976158142090), alpha_hi = static_cast<float>(alpha * 1.00000023841857910);
+  // two scores per packed fp16 word, exact (falls back to f16_dequant when a bracket is open)
+  auto dequant2 = [&](int a0, int a1) -> uint32_t {
+    const float y0 = static_cast<float>(a0), y1 = static_cast<float>(a1);
+    const __half2 l = __floats2half2_rn(y0 * alpha_lo, y1 * alpha_lo);
+    const __half2 h = __floats2half2_rn(y0 * alpha_hi, y1 * alpha_hi);
+    const uint32_t lb = *reinterpret_cast<const uint32_t*>(&l), hb = *reinterpret_cast<const uint32_t*>(&h);
+    if (lb == hb) return lb;
+    return static_cast<uint32_t>(f16_dequant(a0, alpha, alpha_f)) | (static_cast<uint32_t>(f16_dequant(a1, alpha, alpha_f)) << 16);
+  };
+
   // scores of blocks [j0, j0 + jn) into sc[(j - j0) * 8 + v]: the chunk's column indices
-  // are staged in shared memory by one coalesced pass, then the K rows of 4 groups of 16
-  // blocks are loaded before their MMAs (8 independent 16-byte loads in flight per lane)
+  // are staged in shared memory by one coalesced pass (padded with column 0 to a multiple
+  // of 32 for the MIX gathers), then the K rows of 4 groups of 16 blocks are loaded before
+  // their MMAs (8 independent 16-byte loads in flight per lane)
   auto compute = [&](int64_t j0, int jn) {
-    for (int i = lane; i < jn; i += 32) {
-      uint32_t c = __ldg(cols + lo + j0 + i);
-      if (c >= static_cast<uint32_t>(L)) {
-        flag_status(status, MC_STATUS_BAD_INDEX);
-        c = 0;
+    const int jpad = (jn + 31) & ~31;
+    for (int i = lane; i < jpad; i += 32) {
+      uint32_t c = 0;
+      if (i < jn) {
+        c = __ldg(cols + lo + j0 + i);
+        if (c >= static_cast<uint32_t>(L)) {
+          flag_status(status, MC_STATUS_BAD_INDEX);
+          c = 0;
+        }
       }
       ix[i] = c;
     }
@@ -396,15 +414,12 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int m0 = grp0 + 16 * u + g, m1 = m0 + 8;
-        if (grp0 + 16 * u >= jn) break;
         int acc[4] = {0, 0, 0, 0};
         mma16832<false, false>(acc, ka[u].x, kb[u].x, ka[u].y, kb[u].y, qv.x, qv.y);  // d 16t + 0..7
         mma16832<false, false>(acc, ka[u].z, kb[u].z, ka[u].w, kb[u].w, qv.z, qv.w);  // d 16t + 8..15
         // c0 = S[block g][query 2t], c1 = [g][2t+1], c2 = [g+8][2t], c3 = [g+8][2t+1]
-        const uint32_t h01 = static_cast<uint32_t>(f16_dequant(acc[0], alpha, alpha_f)) |
-                             (static_cast<uint32_t>(f16_dequant(acc[1], alpha, alpha_f)) << 16);
-        const uint32_t h23 = static_cast<uint32_t>(f16_dequant(acc[2], alpha, alpha_f)) |
-                             (static_cast<uint32_t>(f16_dequant(acc[3], alpha, alpha_f)) << 16);
+        const uint32_t h01 = dequant2(acc[0], acc[1]);
+        const uint32_t h23 = dequant2(acc[2], acc[3]);
         if (m0 < jn) reinterpret_cast<uint32_t*>(sc)[(m0 * 8 + 2 * t) >> 1] = h01;
         if (m1 < jn) reinterpret_cast<uint32_t*>(sc)[(m1 * 8 + 2 * t) >> 1] = h23;
       }
@@ -509,12 +524,35 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
       return q;
     }
   };
+  // levels of rows 2p, 2p+1 of one block as bytes (FAST, smax <= 2047): packed fp32 pairs;
+  // the level is the low byte of fl(p16 * smax + 1.5 * 2^23) (exact: p16 * smax has <= 22 bits)
+  auto level_pair = [&](__half2 x2, int p, uint32_t& qa, uint32_t& qb) {
+    const float2 x = __half22float2(x2);
+    const float pa = att_exp_fast(x.x, mneg[2 * p]) * inv_f[2 * p];
+    const float pb = att_exp_fast(x.y, mneg[2 * p + 1]) * inv_f[2 * p + 1];
+    const __half2 l = __floats2half2_rn(pa * 0.99999952316284180f, pb * 0.99999952316284180f);
+    const __half2 h = __floats2half2_rn(pa * 1.00000047683715820f, pb * 1.00000047683715820f);
+    const float2 fl = __half22float2(l);
+    qa = __float_as_uint(fmaf(fl.x, smax_f, 12582912.0f));
+    qb = __float_as_uint(fmaf(fl.y, smax_f, 12582912.0f));
+    if (*reinterpret_cast<const uint32_t*>(&l) != *reinterpret_cast<const uint32_t*>(&h)) {
+      qa = static_cast<uint32_t>(level(x.x, 2 * p));
+      qb = static_cast<uint32_t>(level(x.y, 2 * p + 1));
+    }
+  };
   if constexpr (MIX) {
     // pass 3 + P x V: per chunk, the int8 probabilities go to pm[v][j]; then k-steps of
     // 32 blocks: V rows col_j (64 B each) gathered into slot order, D^T[n, v] += V^T P^T
     // (mma.sync m16n8k32: M = 16 head dims per MMA, 4 per k-step; N = 8 query rows)
-    const uint8_t* vb = reinterpret_cast<const uint8_t*>(vw + b * head_words);
+    const uint8_t* vbl = reinterpret_cast<const uint8_t*>(vw + b * head_words) + (lane & 3) * 16;
     const uint32_t vring_s = smem_u32(vring);
+    uint32_t goff[2];  // slot * 64 + swizzled chunk of this lane's copies (u even / odd)
+    {
+      const int k0 = lane >> 2, ch = lane & 3;
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        goff[e] = 64 * (4 * (k0 & 3) + (k0 >> 2) + 2 * e) + ((ch * 16) ^ (32 * e));
+    }
     int acc[4][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -525,33 +563,29 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
       if (!cached) { __syncwarp(); compute(j0, jn); }
       const int jpad = (jn + 31) & ~31;
       for (int j = lane; j < jpad; j += 32) {
-        int32_t qv[8];
+        uint32_t qb[8];
 #pragma unroll
-        for (int v = 0; v < 8; ++v) qv[v] = 0;
+        for (int v = 0; v < 8; ++v) qb[v] = 0;
         if (j < jn) {
           const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
-          const __half* hs = reinterpret_cast<const __half*>(&u);
+          const __half2* hs = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
-          for (int v = 0; v < 8; ++v) qv[v] = level(__half2float(hs[v]), v);
+          for (int p = 0; p < 4; ++p) level_pair(hs[p], p, qb[2 * p], qb[2 * p + 1]);
         }
 #pragma unroll
-        for (int v = 0; v < 8; ++v) pm[v * kCap + j] = static_cast<int8_t>(qv[v]);
+        for (int v = 0; v < 8; ++v) pm[v * kCap + j] = static_cast<int8_t>(qb[v]);
       }
       __syncwarp();
       // gather of k-step s into ring slot s & 1: copy u of this lane moves 16-byte chunk
-      // ch of gathered row kk (4 chunks per 64-byte row), slot order + XOR swizzle as spmm.cu
+      // ch = lane & 3 of gathered row kk = lane / 4 + 8u (slot order + XOR swizzle as
+      // spmm.cu; the per-lane slot offsets are hoisted in goff). The column padding of ix
+      // (column 0) pairs with P = 0, so the copies are unconditional.
       auto gather = [&](int s) {
         const uint32_t base = vring_s + (s & 1) * 2048;
+        const uint32_t* ixs = ix + 32 * s + (lane >> 2);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int qq = lane + 32 * u;
-          const int kk = qq >> 2, ch = qq & 3;
-          const int jj = 32 * s + kk;
-          const int slot = ((kk >> 4) << 4) | ((kk & 3) << 2) | ((kk >> 2) & 3);
-          const uint32_t dst = base + slot * 64 + ((ch * 16) ^ (32 * ((slot & 3) >> 1)));
-          const bool ok = jj < jn;
-          cp_async16(dst, ok ? vb + static_cast<int64_t>(ix[jj]) * 64 + ch * 16 : vb, ok ? 16u : 0u);
-        }
+        for (int u = 0; u < 4; ++u)
+          cp_async16_full(base + goff[u & 1] + 1024 * (u >> 1), vbl + static_cast<size_t>(ixs[8 * u]) * 64);
         cp_async_commit();
       };
       const int nsteps = jpad >> 5;
