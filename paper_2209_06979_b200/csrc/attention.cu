@@ -328,12 +328,16 @@ __global__ void quant8_f16_kernel(const __half* q, const __half* k, const __half
 // through the same float64 max / exp-sum / prob / requant sequence as
 // softmax_requant_kernel, which writes the SR-BCRS probability values the SpMM consumes.
 // Saves the fp16 score round trip through HBM and the score kernel's K = 64 padding.
-constexpr int kAttCap = 512;  // cached mask blocks per warp (8 KB of fp16 scores)
+// cached mask blocks per warp (fp16 scores [kCap][8]); MIX trims it so that four 4-warp
+// CTAs fit an SM (16 warps)
+template <bool MIX>
+constexpr int att_cap() { return MIX ? 480 : 512; }
 // per-warp shared memory of the fused kernel: scores [kCap][8] fp16, column indices
-// [kCap], and with MIX the int8 probabilities [8][kCap] + a 2-slot ring of 32 V rows
+// [kCap], the row sums (float64, for the rare exact-division fallback), and with MIX the
+// int8 probabilities of one k-step [8][32] + a 2-slot ring of 32 V rows
 template <bool MIX>
 constexpr int att_warp_smem() {
-  return kAttCap * 16 + kAttCap * 4 + (MIX ? kAttCap * 8 + 2 * 32 * 64 : 0);
+  return att_cap<MIX>() * 20 + 64 + (MIX ? 8 * 32 + 2 * 32 * 64 : 0);
 }
 
 // MIX: also the P x V product (attention.py:164-176) -- the requantised probabilities stay
@@ -342,21 +346,22 @@ constexpr int att_warp_smem() {
 // and the output is dequantised to fp16 in the epilogue (one kernel per layer after
 // quantisation); otherwise pass 3 writes the SR-BCRS probabilities for the SpMM kernel.
 template <bool FAST, bool MIX>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, (MIX && FAST) ? 4 : 1)
 score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict__ kw, int64_t head_words,
                      const int64_t* __restrict__ offs, const uint32_t* __restrict__ cols, int64_t vrows,
                      int64_t L, const double* __restrict__ alpha_s, const int64_t* __restrict__ sr_begin, int S,
                      int smax, int sbits, uint32_t* sr_vals, int64_t sr_stride_words, int64_t batch,
                      uint32_t* status, const uint32_t* __restrict__ vw, const double* __restrict__ alpha_m,
                      uint16_t* __restrict__ out_f16) {
-  constexpr int kCap = kAttCap;
+  constexpr int kCap = att_cap<MIX>();
   extern __shared__ __align__(16) uint8_t att_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* wsm = att_smem + warp * att_warp_smem<MIX>();
   uint16_t* sc = reinterpret_cast<uint16_t*>(wsm);
   uint32_t* ix = reinterpret_cast<uint32_t*>(wsm + kCap * 16);
-  int8_t* pm = reinterpret_cast<int8_t*>(wsm + kCap * 20);        // MIX: P[v][kCap]
-  uint8_t* vring = wsm + kCap * 28;                               // MIX: 2 x 32 V rows x 64 B
+  double* wsum = reinterpret_cast<double*>(wsm + kCap * 20);      // row sums [8]
+  int8_t* pm = reinterpret_cast<int8_t*>(wsm + kCap * 20 + 64);   // MIX: P[v][32] of one k-step
+  uint8_t* vring = wsm + kCap * 20 + 64 + 256;                    // MIX: 2 x 32 V rows x 64 B
   const int g = lane >> 2, t = lane & 3;
   if (threadIdx.x == 0) pdl_launch_dependents();
   pdl_wait();
@@ -501,6 +506,7 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
     for (int o = 16; o > 0; o >>= 1) sum[v] += __shfl_xor_sync(0xffffffffu, sum[v], o);
     inv_sum[v] = 1.0 / sum[v];
     inv_f[v] = static_cast<float>(inv_sum[v]);
+    if (lane == 0) wsum[v] = sum[v];
     // requant level q >= 1 needs p16 * smax >= 0.5, i.e. p > 0.4998 / smax, i.e.
     // x - max > ln(0.4998 * sum / smax); below the (10 % lower) threshold q is exactly 0
     thr[v] = mxf[v] + static_cast<float>(log(0.45 * sum[v] / static_cast<double>(smax)));
@@ -510,9 +516,10 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
     if constexpr (FAST) {
       const float e = att_exp_fast(xf, mneg[v]);
       int q = prob_q_fast(e, inv_f[v], smax_f);
-      if (q < 0) {
+      if (q < 0) {  // rare: the float64 chain with the row sum kept in shared memory
         uint16_t pf;
-        prob_requant(static_cast<double>(e), sum[v], inv_sum[v], smax, pf, q);
+        const double sv = wsum[v];
+        prob_requant(static_cast<double>(e), sv, 1.0 / sv, smax, pf, q);
       }
       return q;
     } else {
@@ -562,20 +569,6 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
       const int jn = static_cast<int>(nb - j0 < kCap ? nb - j0 : kCap);
       if (!cached) { __syncwarp(); compute(j0, jn); }
       const int jpad = (jn + 31) & ~31;
-      for (int j = lane; j < jpad; j += 32) {
-        uint32_t qb[8];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) qb[v] = 0;
-        if (j < jn) {
-          const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
-          const __half2* hs = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-          for (int p = 0; p < 4; ++p) level_pair(hs[p], p, qb[2 * p], qb[2 * p + 1]);
-        }
-#pragma unroll
-        for (int v = 0; v < 8; ++v) pm[v * kCap + j] = static_cast<int8_t>(qb[v]);
-      }
-      __syncwarp();
       // gather of k-step s into ring slot s & 1: copy u of this lane moves 16-byte chunk
       // ch = lane & 3 of gathered row kk = lane / 4 + 8u (slot order + XOR swizzle as
       // spmm.cu; the per-lane slot offsets are hoisted in goff). The column padding of ix
@@ -592,6 +585,21 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
       gather(0);
       for (int s_ = 0; s_ < nsteps; ++s_) {
         if (s_ + 1 < nsteps) gather(s_ + 1);
+        // pass 3 for the k-step's blocks (overlaps the gathers): levels of block 32 s + lane
+        {
+          const int j = 32 * s_ + lane;
+          uint32_t qb[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) qb[v] = 0;
+          if (j < jn) {
+            const uint4 u = *reinterpret_cast<const uint4*>(sc + j * 8);
+            const __half2* hs = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) level_pair(hs[p], p, qb[2 * p], qb[2 * p + 1]);
+          }
+#pragma unroll
+          for (int v = 0; v < 8; ++v) pm[v * 32 + lane] = static_cast<int8_t>(qb[v]);
+        }
         if (s_ + 1 < nsteps) cp_async_wait<1>();
         else cp_async_wait<0>();
         __syncwarp();
@@ -599,7 +607,7 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
         // B operand: P[g][32 s + 16 h + 4 t .. +3]
         uint32_t bf[2];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) bf[h] = *reinterpret_cast<const uint32_t*>(pm + g * kCap + 32 * s_ + 16 * h + 4 * t);
+        for (int h = 0; h < 2; ++h) bf[h] = *reinterpret_cast<const uint32_t*>(pm + g * 32 + 16 * h + 4 * t);
         // A operand: gathered rows, transposed to k-major words per head dim
         uint32_t T[2][8];
 #pragma unroll
