@@ -144,6 +144,11 @@ __device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsig
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 __device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
   unsigned long long r;
   asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
@@ -233,91 +238,158 @@ __global__ void softmax_requant_kernel(const uint16_t* __restrict__ scores, int6
 
 // ---- fp16-input fast paths (the C4 configuration) ----
 
-// grid (batch * splits, 3): |x| max of a slice of one [L x d] fp16 tensor, combined with an
-// integer atomicMax on the float bit pattern (non-negative floats order like their bits).
-// Exact: the maximum of fp16 magnitudes is representable in fp32.
-__global__ void __launch_bounds__(256)
-absmax_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n, int splits, uint32_t* amax_bits) {
-  const int64_t b = blockIdx.x / splits;
-  const int sp = blockIdx.x - static_cast<int>(b * splits);
-  const int which = blockIdx.y;
-  const __half* src = (which == 0 ? q : (which == 1 ? k : v)) + b * n;
-  const int64_t n8 = n / 8;
-  const int64_t c0 = (n8 * sp) / splits, c1 = (n8 * (sp + 1)) / splits;
-  float m = 0.f;
-  for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-    const uint4 u = __ldg(reinterpret_cast<const uint4*>(src) + c);
-    const __half2* h = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const float2 f = __half22float2(h[x]);
-      m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
-    }
-  }
-  if (sp == splits - 1)  // tail elements (n not a multiple of 8)
-    for (int64_t i = n8 * 8 + threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, fabsf(__half2float(src[i])));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits + b * 3 + which, __float_as_uint(m));
-}
-
-// scales (attention.py:52-54) and the two dequant factors (:147, :169) per head
-__global__ void scales_kernel(const uint32_t* amax_bits, int64_t batch, int bits, int smax, int head_dim,
-                              double* scales, double* alpha_s, double* alpha_m) {
-  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  const double qmax = static_cast<double>((1 << (bits - 1)) - 1);
-  double sc[3];
-#pragma unroll
-  for (int w = 0; w < 3; ++w) {
-    const double m = static_cast<double>(__uint_as_float(amax_bits[b * 3 + w]));
-    sc[w] = m > 0.0 ? m / qmax : 1.0;
-    scales[b * 4 + w] = sc[w];
-  }
-  const double ss = 1.0 / static_cast<double>(smax);
-  scales[b * 4 + 3] = ss;
-  alpha_s[b] = sc[0] * sc[1] / sqrt(static_cast<double>(head_dim));
-  alpha_m[b] = ss * sc[2];
-}
-
-// 8-bit quantisation of fp16 inputs, 16 elements (one 16-byte output) per thread.
-// FAST: float32 (x / scale rounded half-to-even); otherwise float64 as attention.py:55.
-template <bool FAST>
-__global__ void quant8_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n,
-                                  const double* scales, uint32_t* out, int64_t words_per, int64_t batch) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // 16-element group
-  const int which = blockIdx.y;
-  const int64_t groups = n / 16;
-  if (t >= groups * batch) return;
-  const int64_t b = t / groups, g = t - b * groups;
-  const __half* src = (which == 0 ? q : (which == 1 ? k : v)) + b * n + g * 16;
-  const double scale = scales[b * 4 + which];
-  const float scale_f = static_cast<float>(scale);
-  const uint4 u0 = __ldg(reinterpret_cast<const uint4*>(src)), u1 = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+// 8-bit quantisation of 16 fp16 values into one 16-byte output (attention.py:55):
+// q = clip(rint(x / scale)) with the quotient in float64.
+__device__ __forceinline__ uint4 quant16_f16_exact(uint4 u0, uint4 u1, double scale) {
   const __half* h = reinterpret_cast<const __half*>(&u0);
   const __half* h1 = reinterpret_cast<const __half*>(&u1);
   uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
-    const __half x = e < 8 ? h[e] : h1[e - 8];
-    // q = clip(rint(x / scale)) in float64 (attention.py:55). The fp32 quotient is within
-    // 2^-20 relative of it, so it decides rint exactly unless it lies within 2^-12 of a
-    // rounding tie; those (rare) elements take the float64 division.
-    int qi;
-    const float xf = __half2float(x);
-    const float qf = xf / scale_f;
-    const float fr = fabsf(qf - truncf(qf));
-    if (!FAST || fabsf(fr - 0.5f) < 2.4e-4f) {
-      double d = rint(static_cast<double>(xf) / scale);
-      qi = static_cast<int>(fmin(fmax(d, -127.0), 127.0));
-    } else {
-      qi = static_cast<int>(rintf(qf));
-      qi = qi > 127 ? 127 : (qi < -127 ? -127 : qi);
-    }
+    const double d = rint(static_cast<double>(__half2float(e < 8 ? h[e] : h1[e - 8])) / scale);
+    const int qi = static_cast<int>(fmin(fmax(d, -127.0), 127.0));
     w[e >> 2] |= (static_cast<uint32_t>(qi) & 0xFFu) << (8 * (e & 3));
   }
-  *reinterpret_cast<uint4*>(out + (static_cast<int64_t>(which) * batch + b) * words_per + g * 4) =
-      make_uint4(w[0], w[1], w[2], w[3]);
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// FAST: the quotient as x * fp32(1 / scale) (packed FMUL2) is within 2^-23 relative
+// (<= 1.6e-5 absolute for |q| <= 127.5) of the float64 one, so rounding it (magic-number
+// FADD2, whose low byte is the two's-complement level) gives the float64 result unless it
+// lies within 5e-5 of a tie; a group with such an element takes quant16_f16_exact. The
+// level never exceeds 127 in magnitude (|x| <= absmax = 127 * scale), so no clip is needed.
+template <bool FAST>
+__device__ __forceinline__ uint4 quant16_f16(uint4 u0, uint4 u1, double scale, float inv_f) {
+  if constexpr (!FAST) {
+    return quant16_f16_exact(u0, u1, scale);
+  } else {
+    const uint4 uu[2] = {u0, u1};
+    const unsigned long long inv2 = f2_pack(inv_f, inv_f), mag2 = f2_pack(12582912.0f, 12582912.0f);
+    uint32_t w[4];
+    float dmax = 0.f;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const __half2* h = reinterpret_cast<const __half2*>(&uu[i]);
+      uint32_t tb[8];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const float2 f = __half22float2(h[x]);
+        const unsigned long long qf = f2_mul(f2_pack(f.x, f.y), inv2);
+        const unsigned long long tq = f2_add(qf, mag2);
+        const float2 dd = f2_unpack(f2_sub(qf, f2_sub(tq, mag2)));
+        dmax = fmaxf(dmax, fmaxf(fabsf(dd.x), fabsf(dd.y)));
+        const float2 tt = f2_unpack(tq);
+        tb[2 * x] = __float_as_uint(tt.x);
+        tb[2 * x + 1] = __float_as_uint(tt.y);
+      }
+      w[2 * i] = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+      w[2 * i + 1] = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
+    }
+    if (dmax > 0.49995f) return quant16_f16_exact(u0, u1, scale);
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// One 8-CTA cluster per [L x d] fp16 tensor (grid (8 * batch, 3) = Q, K, V of each head):
+// each CTA holds its 1/8 slice in registers, the slice maxima meet through distributed
+// shared memory (|x| max, attention.py:52-54; exact in fp32 for fp16 magnitudes), and the
+// slice is quantised from registers -- one HBM read and one int8 write per element. The
+// last of a head's three rank-0 CTAs (per-head arrival counter, reset for the next launch)
+// derives alpha_s (:147) and alpha_m (:169).
+constexpr int kQuantThreads = 512, kQuantCluster = 8, kQuantVec = 8;  // 8 x 16 B per thread
+__device__ __forceinline__ void st_cluster_f32(const float* local_addr, uint32_t rank, float v) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local_addr)), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <bool FAST>
+__global__ void __cluster_dims__(kQuantCluster, 1, 1) __launch_bounds__(kQuantThreads, 2)
+absquant_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n, int smax, int head_dim,
+                    double* scales, double* alpha_s, double* alpha_m, uint32_t* out, int64_t words_per,
+                    int64_t batch, uint32_t* arrivals) {
+  __shared__ float red[kQuantThreads / 32];
+  __shared__ float slice_max[kQuantCluster];
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int64_t b = blockIdx.x / kQuantCluster;
+  const int which = blockIdx.y;
+  const uint4* src = reinterpret_cast<const uint4*>((which == 0 ? q : (which == 1 ? k : v)) + b * n);
+  uint4* dst = reinterpret_cast<uint4*>(out + (static_cast<int64_t>(which) * batch + b) * words_per);
+  // slice: 16-element groups [g0, g1) of this CTA; group g = 2 uint4 of input, 1 of output
+  const int64_t n16 = n / 16;
+  const int64_t g0 = n16 * rank / kQuantCluster, g1 = n16 * (rank + 1) / kQuantCluster;
+  uint4 u[kQuantVec];
+  float m = 0.f;
+  __half2 m2 = __float2half2_rn(0.f);
+#pragma unroll
+  for (int i = 0; i < kQuantVec / 2; ++i) {
+    const int64_t g = g0 + threadIdx.x + static_cast<int64_t>(i) * kQuantThreads;
+    const bool ok = g < g1;
+    u[2 * i] = ok ? __ldg(src + 2 * g) : make_uint4(0u, 0u, 0u, 0u);
+    u[2 * i + 1] = ok ? __ldg(src + 2 * g + 1) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  // slices larger than the register tile (n > 8 * 16 * 512 * 4) are streamed twice
+  for (int64_t g = g0 + threadIdx.x + static_cast<int64_t>(kQuantVec / 2) * kQuantThreads; g < g1; g += kQuantThreads) {
+    const uint4 w[2] = {__ldg(src + 2 * g), __ldg(src + 2 * g + 1)};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const __half2* h = reinterpret_cast<const __half2*>(&w[i]);
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        const float2 f = __half22float2(h[x]);
+        m = fmaxf(m, fmaxf(fabsf(f.x), fabsf(f.y)));
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kQuantVec; ++i) {
+    const __half2* h = reinterpret_cast<const __half2*>(&u[i]);
+#pragma unroll
+    for (int x = 0; x < 4; ++x) m2 = __hmax2(m2, __habs2(h[x]));  // exact on fp16
+  }
+  {
+    const float2 f = __half22float2(m2);
+    m = fmaxf(m, fmaxf(f.x, f.y));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < kQuantThreads / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x < kQuantCluster) st_cluster_f32(&slice_max[rank], threadIdx.x, m);  // to every CTA
+  }
+  cluster_barrier();  // no remote shared-memory access after this point
+  m = 0.f;
+#pragma unroll
+  for (int i = 0; i < kQuantCluster; ++i) m = fmaxf(m, slice_max[i]);
+  const double md = static_cast<double>(m);
+  const double scale = md > 0.0 ? md / 127.0 : 1.0;
+  const float inv_f = static_cast<float>(1.0 / scale);
+#pragma unroll
+  for (int i = 0; i < kQuantVec / 2; ++i) {
+    const int64_t g = g0 + threadIdx.x + static_cast<int64_t>(i) * kQuantThreads;
+    if (g < g1) dst[g] = quant16_f16<FAST>(u[2 * i], u[2 * i + 1], scale, inv_f);
+  }
+  for (int64_t g = g0 + threadIdx.x + static_cast<int64_t>(kQuantVec / 2) * kQuantThreads; g < g1; g += kQuantThreads)
+    dst[g] = quant16_f16<FAST>(__ldg(src + 2 * g), __ldg(src + 2 * g + 1), scale, inv_f);
+  if (rank == 0 && threadIdx.x == 0) {
+    scales[b * 4 + which] = scale;
+    uint32_t prev;  // release publishes the scale, acquire (for the last) sees the others'
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(arrivals + b) : "memory");
+    if (prev == 2u) {
+      const double s0 = __ldcg(scales + b * 4), s1 = __ldcg(scales + b * 4 + 1), s2 = __ldcg(scales + b * 4 + 2);
+      const double ss = 1.0 / static_cast<double>(smax);
+      scales[b * 4 + 3] = ss;
+      alpha_s[b] = s0 * s1 / sqrt(static_cast<double>(head_dim));
+      alpha_m[b] = ss * s2;
+      arrivals[b] = 0u;
+    }
+  }
 }
 
 // Fused score SDDMM + softmax + requant for 8-bit Q/K and d = 64 (attention.py:147-162):
@@ -726,26 +798,13 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
   const bool fast = a->mode == MC_ATTN_FAST;
   if (a->in_dtype == MC_DTYPE_F16 && qb == 8 && n % 16 == 0 && (reinterpret_cast<uintptr_t>(a->q) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(a->k) & 15) == 0 && (reinterpret_cast<uintptr_t>(a->v) & 15) == 0) {
-    // vectorised fp16 path: split absmax (atomicMax on float bits) -> scales -> 16-wide quant
-    uint32_t* amax = reinterpret_cast<uint32_t*>(ws + o_amax);
-    cudaMemsetAsync(amax, 0, B * 3 * 4, stream);
-    const int splits = static_cast<int>(n / 8 >= 8 * 256 ? 8 : 1);
-    absmax_f16_kernel<<<dim3(static_cast<unsigned>(B * splits), 3), 256, 0, stream>>>(
-        static_cast<const __half*>(a->q), static_cast<const __half*>(a->k), static_cast<const __half*>(a->v), n, splits,
-        amax);
-    count_launch();
-    scales_kernel<<<static_cast<unsigned>((B + 127) / 128), 128, 0, stream>>>(amax, B, qb, smax, a->head_dim, scales,
-                                                                             alpha_s, alpha_m);
-    count_launch();
-    const unsigned qgrid = static_cast<unsigned>((B * (n / 16) + 255) / 256);
-    if (fast)
-      quant8_f16_kernel<true><<<dim3(qgrid, 3), 256, 0, stream>>>(
-          static_cast<const __half*>(a->q), static_cast<const __half*>(a->k), static_cast<const __half*>(a->v), n,
-          scales, qkv, qwords, B);
-    else
-      quant8_f16_kernel<false><<<dim3(qgrid, 3), 256, 0, stream>>>(
-          static_cast<const __half*>(a->q), static_cast<const __half*>(a->k), static_cast<const __half*>(a->v), n,
-          scales, qkv, qwords, B);
+    // vectorised fp16 path: one kernel (absmax, scale, 16-wide quant, alphas) per tensor
+    uint32_t* arrivals = reinterpret_cast<uint32_t*>(ws + o_amax);
+    cudaMemsetAsync(arrivals, 0, B * 4, stream);
+    auto kq = fast ? absquant_f16_kernel<true> : absquant_f16_kernel<false>;
+    kq<<<dim3(static_cast<unsigned>(B * kQuantCluster), 3), kQuantThreads, 0, stream>>>(
+        static_cast<const __half*>(a->q), static_cast<const __half*>(a->k), static_cast<const __half*>(a->v), n, smax,
+        a->head_dim, scales, alpha_s, alpha_m, qkv, qwords, B, arrivals);
     count_launch();
   } else {
     absmax_kernel<<<dim3(static_cast<unsigned>(B), 3), 512, 0, stream>>>(a->q, a->k, a->v, a->in_dtype, n, qb,
