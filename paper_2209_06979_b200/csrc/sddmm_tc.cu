@@ -74,11 +74,11 @@ struct __align__(16) QuarterMap {
   long long pos;
 };
 
-template <int V>
+template <int V, int VR_>
 struct Lay {
-  static constexpr int VR = kVRows;
-  static constexpr int PANEL = kVRows * V;  // scalar rows of A per tile (UMMA N, TMEM columns)
-  static constexpr int STAGES = V == 8 ? 2 : 3;  // B^T tile ring depth (smem budget)
+  static constexpr int VR = VR_;  // vector rows per tile (32, or 16 for finer load balance)
+  static constexpr int PANEL = VR_ * V;  // scalar rows of A per tile (UMMA N, TMEM columns)
+  static constexpr int STAGES = (V == 8 && VR_ == 32) ? 2 : 3;  // B^T tile ring depth (smem budget)
   static constexpr int A_BYTES = PANEL * 256;  // K <= 256
   static constexpr int B_STAGE = kCols * 256;
   static constexpr int MAP = VR * 4 * 16;
@@ -158,14 +158,15 @@ struct TileCursor {
   }
 };
 
-template <int V>
+template <int V, int VR_>
 __global__ void __launch_bounds__(kThreads, 1)
 sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const SddmmTcParams p) {
-  using L = Lay<V>;
+  using L = Lay<V, VR_>;
   constexpr int kStages = L::STAGES;
   constexpr int VR = L::VR;
   constexpr int PANEL = L::PANEL;
+  constexpr int kBW = VR / kRowsPerBuilder;  // active builder warps (the rest idle when VR = 16)
   constexpr uint32_t kIdesc = tc::idesc_i8(128, PANEL);
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // align to 1024 B (SW128 atoms) with pointer arithmetic (keeps the shared window)
@@ -249,7 +250,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       tc::mbar_init(tempty_bar(a), kConsWarps);
     }
     for (int s = 0; s < kRing; ++s) {
-      tc::mbar_init(pfull_bar(s), kBuildWarps);  // one arrival per builder warp
+      tc::mbar_init(pfull_bar(s), kBW);  // one arrival per active builder warp
       tc::mbar_init(pempty_bar(s), kConsWarps);
     }
     tc::fence_barrier_init();
@@ -270,7 +271,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         tc::tma_prefetch_2d(&tmA, kb * KBLK, static_cast<int>(c.item * p.M + c.panel * PANEL));
         tc::tma_prefetch_2d(&tmB, kb * KBLK, static_cast<int>(c.item * p.N + c.ct * kCols));
       }
-    } else if (warp >= kFirstBuild && warp < kFirstCons && (lane & (kLanesPerRow - 1)) == 0) {
+    } else if (warp >= kFirstBuild && warp < kFirstBuild + kBW && (lane & (kLanesPerRow - 1)) == 0) {
       const long long r = c.panel * VR + rl;
       if (r < p.vrows) {
         tc::prefetch_l2(p.row_offsets + r);
@@ -287,7 +288,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   int mtop_last = 0;  // chunk bound of all cp.async groups but the most recent one
   long long b_r = -1;
   uint32_t b_c00 = 0;
-  if (warp >= kFirstBuild && warp < kFirstCons && t0 < t1) {
+  if (warp >= kFirstBuild && warp < kFirstBuild + kBW && t0 < t1) {
     const int64_t rem0 = t0 % tiles_per_item;
     b_r = (rem0 / p.n_ctiles) * VR + rl;
     b_c00 = static_cast<uint32_t>((rem0 % p.n_ctiles) * kCols);
@@ -370,7 +371,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (t + 1 == t1 || tc_.ct + 1 == p.n_ctiles) tc::mma_commit(a_empty);  // panel's last tile
       }
     }
-  } else if (warp < kFirstCons) {
+  } else if (warp < kFirstBuild + kBW) {
     // ---------------- pattern builders (4 independent warps) ----------------
     // Builder warp bw owns vector rows 4*bw .. 4*bw+3 of the tile; lane = (row j, sub s),
     // eight lanes per row. Each row streams its CSR column list through a 512-entry ring
@@ -555,7 +556,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       MC_STAMP(lane == 0 && bw == 0 && i < 6, 22 + 3 * static_cast<int>(i));
     }
     cp_async_wait<0>();
-  } else {
+  } else if (warp >= kFirstCons) {
     // ---------------- consumers: TMEM -> registers -> V*4-byte block stores ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = (warp - kFirstCons) >> 2;
@@ -692,8 +693,12 @@ bool sddmm_tc_supported(const SddmmParams& p) {
 }
 
 cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream) {
+  // tile height: 32 vector rows; 16 (MCUBE_SDDMM_VR=16) halves the per-tile epilogue for a
+  // finer last wave but measured slower at every C2 density (per-tile costs dominate)
+  int vr = 32;
+  if (const char* e = getenv("MCUBE_SDDMM_VR")) vr = atoi(e) == 16 ? 16 : 32;
   CUtensorMap ta, tb;
-  if (!make_map(&ta, p.a_words, p.batch * p.M, p.K, kVRows * p.V) || !make_map(&tb, p.b_words, p.batch * p.N, p.K, kCols))
+  if (!make_map(&ta, p.a_words, p.batch * p.M, p.K, vr * p.V) || !make_map(&tb, p.b_words, p.batch * p.N, p.K, kCols))
     return cudaErrorInvalidValue;
   SddmmTcParams q{};
   q.M = p.M;
@@ -711,7 +716,7 @@ cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream) {
   q.out_f16 = p.out_f16;
   q.f16_stride = p.f16_stride;
   q.status = p.status;
-  q.n_panels = static_cast<int>((p.M + kVRows * p.V - 1) / (kVRows * p.V));
+  q.n_panels = static_cast<int>((p.M + vr * p.V - 1) / (vr * p.V));
   q.n_ctiles = static_cast<int>((p.N + kCols - 1) / kCols);
   q.tiles = static_cast<int64_t>(p.batch) * q.n_panels * q.n_ctiles;
   q.debug = getenv("MCUBE_DEBUG_TIMELINE") != nullptr;
@@ -720,11 +725,14 @@ cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = static_cast<int>(q.tiles < sms ? q.tiles : sms);
   if (grid == 0) return cudaSuccess;
-  decltype(&sddmm_tc_kernel<8>) kern;
+  decltype(&sddmm_tc_kernel<8, 32>) kern;
   int smem;
-  switch (p.V) {
-    case 8: kern = sddmm_tc_kernel<8>; smem = Lay<8>::TOTAL; break;
-    default: kern = sddmm_tc_kernel<4>; smem = Lay<4>::TOTAL; break;
+  if (p.V == 8) {
+    kern = vr == 16 ? sddmm_tc_kernel<8, 16> : sddmm_tc_kernel<8, 32>;
+    smem = vr == 16 ? Lay<8, 16>::TOTAL : Lay<8, 32>::TOTAL;
+  } else {
+    kern = vr == 16 ? sddmm_tc_kernel<4, 16> : sddmm_tc_kernel<4, 32>;
+    smem = vr == 16 ? Lay<4, 16>::TOTAL : Lay<4, 32>::TOTAL;
   }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const cudaError_t e = launch_pdl(kern, dim3(grid), dim3(kThreads), smem, stream, ta, tb, q);
