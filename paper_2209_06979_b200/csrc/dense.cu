@@ -120,14 +120,17 @@ densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restri
       }
     }
   }
+  // copy-out by the bulk-copy engine: one kc-byte row per plane row (kc % 16 == 0 and
+  // 16-byte aligned rows: the dense path requires K % 128 == 0)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  // coalesced copy-out: 16-byte vectors of each of the LC * V rows
-  const int per_row = kc / 16;
-  for (int i = threadIdx.x; i < LC * V * per_row; i += blockDim.x) {
-    const int rowp = i / per_row, x = i - rowp * per_row;
-    const int pl = rowp / V, v = rowp - pl * V;
-    int8_t* dst = (pl == 0 ? plane0 : plane1) + (r * V + v) * p.K + k0 + 16 * x;
-    *reinterpret_cast<uint4*>(dst) = sm4[(rowp * kKC) / 16 + x];
+  if (threadIdx.x < LC * V) {
+    const int pl = threadIdx.x / V, v = threadIdx.x - pl * V;
+    int8_t* dst = (pl == 0 ? plane0 : plane1) + (r * V + v) * p.K + k0;
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(sm + threadIdx.x * kKC)), "r"(static_cast<uint32_t>(kc)) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
 }
 
