@@ -53,7 +53,7 @@ __device__ __forceinline__ void stamp(bool on, int slot) {
 
 namespace {
 
-constexpr int kVRows = 32;    // vector rows per tile: 32*V scalar rows of A (UMMA N)
+
 constexpr int kCols = 128;   // pattern columns per tile (UMMA M)
 constexpr int kRing = 4;     // pattern-map ring (power of two: slot = i & 3, phase = i >> 2)
 constexpr int kBuildWarps = 8;
