@@ -485,3 +485,23 @@ def test_spmm_dense_path_k_beyond_one_densify_chunk(pair, monkeypatch):
     want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], 8, c["stride"],
                   c["shuffled"], lb, c["rhs"], rb, n)
     assert (np.asarray(out) == want).all()
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_attention_long_sequence_streams_quant_slices(mode):
+    """L = 8192: each quantisation CTA's slice (8 per tensor) exceeds its register tile, so the
+    streaming second pass of absquant_f16_kernel runs; the fused kernel's rows (1638 blocks at
+    80 %) exceed its shared-memory cache (recompute path)."""
+    import torch
+    L, d, heads, sp = 8192, 64, 1, 0.8
+    a = O.build_attention_case(L, d, sp, seed=8192)
+    offs, cols = a["offsets"], a["col_indices"]
+    mask = mc.BcrsMatrix(L, L, 8, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * 8), 8))
+    cfg = mc.AttentionConfig(L, 8, 8, mask, head_dim=d, num_heads=heads)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v = (torch.randn((heads, L, d), device="cuda", generator=g).half() for _ in range(3))
+    out = mc.AttentionRunner(cfg, heads, mode=mode)(q, k, v, check=True).clone()
+    qh, kh, vh = (x[0].double().cpu().numpy() for x in (q, k, v))
+    ref = O.attention(qh, kh, vh, offs, cols, L, d, 8, 8)
+    err = float(np.abs(out[0].double().cpu().numpy() - ref["output"]).max())
+    assert err <= (0.0 if mode == "parity" else mc.attention.FAST_MODE_TOLERANCE), err
