@@ -446,6 +446,7 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
   // query rows r*8 .. r*8+7 (MMA N = 8): this thread's 16 bytes d = 16t .. 16t+15 of row g
   const uint4 qv = __ldg(reinterpret_cast<const uint4*>(qw + b * head_words + (r * 8 + g) * 16) + t);
   const uint32_t* kh = kw + b * head_words;
+  const uint8_t* khb = reinterpret_cast<const uint8_t*>(kh) + t * 16;  // this lane's 16 bytes of a K row
 
   // dequantisation brackets: fp16 of acc * alpha_{lo,hi} (alpha * (1 -+ 2^-22) in fp32) brackets
   // fp16(acc * alpha) (fp32 error <= 2^-23); equal ends are the exact f16_dequant result
@@ -485,8 +486,8 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
         const int m0 = grp0 + 16 * u + g, m1 = m0 + 8;
         const uint32_t c_lo = m0 < jn ? ix[m0] : 0u;
         const uint32_t c_hi = m1 < jn ? ix[m1] : 0u;
-        ka[u] = __ldg(reinterpret_cast<const uint4*>(kh + static_cast<int64_t>(c_lo) * 16) + t);
-        kb[u] = __ldg(reinterpret_cast<const uint4*>(kh + static_cast<int64_t>(c_hi) * 16) + t);
+        ka[u] = __ldg(reinterpret_cast<const uint4*>(khb + static_cast<size_t>(c_lo) * 64));
+        kb[u] = __ldg(reinterpret_cast<const uint4*>(khb + static_cast<size_t>(c_hi) * 64));
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
