@@ -307,7 +307,10 @@ bool dense_spmm_eligible(const SpmmParams& p) {
   const char* e = getenv("MCUBE_SPMM_PATH");
   if (e && e[0] == 'd') return true;   // forced dense
   if (e && e[0] != 'd') return false;  // forced gather (mma / tc)
-  return density >= 0.08;  // C3 crossover: 26.6 us dense vs 28.6 us gather at 10 %
+  // C3 crossover: 24.5 us dense vs 28.6 us gather at 10 %; with fewer than 64 output tiles
+  // the GEMM cannot fill the GPU (C1, 8 tiles: 14.3 us dense vs 8.2 us gather)
+  const long long tiles = (p.M / kTM) * (p.N / 128);
+  return density >= 0.08 && tiles >= 64;
 }
 
 cudaError_t launch_gemm_tc(const SpmmParams& p, const int8_t* a0, const int8_t* a1, const int8_t* b0,
