@@ -307,10 +307,14 @@ bool dense_spmm_eligible(const SpmmParams& p) {
   const char* e = getenv("MCUBE_SPMM_PATH");
   if (e && e[0] == 'd') return true;   // forced dense
   if (e && e[0] != 'd') return false;  // forced gather (mma / tc)
-  // C3 crossover: 24.5 us dense vs 28.6 us gather at 10 %; with fewer than 64 output tiles
-  // the GEMM cannot fill the GPU (C1, 8 tiles: 14.3 us dense vs 8.2 us gather)
+  // The gather moves one RHS row per stored vector (bytes ~ density / V), the dense pass a
+  // fixed M*K + GEMM: measured C3 crossovers (tools/c3_path_probe.py, 5 pairs x V in
+  // {2, 4, 8} x 95/98 %) sit at density / V ~ 0.008 (L16-R16), 0.012 (other 2-plane LHS)
+  // and 0.010 (8/4-bit LHS). With fewer than 64 output tiles the GEMM cannot fill the GPU
+  // (C1, 8 tiles: 14.3 us dense vs 8.2 us gather).
   const long long tiles = (p.M / kTM) * (p.N / 128);
-  return density >= 0.08 && tiles >= 64;
+  const double thr = p.LB >= 12 ? (p.RB == 16 ? 0.008 : 0.012) : 0.010;
+  return density / p.V >= thr && tiles >= 64;
 }
 
 cudaError_t launch_gemm_tc(const SpmmParams& p, const int8_t* a0, const int8_t* a1, const int8_t* b0,
