@@ -112,11 +112,8 @@ sddmm_kernel(const SddmmParams p) {
   const float alpha_f = static_cast<float>(alpha);
   bool overflow = false;
 
-  for (int64_t gi = gbeg; gi < gend; ++gi) {
-    const int64_t blk0 = lo + gi * 16;
-    const int nvalid = static_cast<int>(min_i64(16, hi - blk0));
-    uint32_t mycol = (gi == gbeg && spec_ok) ? spec_col
-                                             : ((lane < nvalid) ? __ldg(p.col_indices + blk0 + lane) : 0u);
+  // one group of 16 pattern blocks starting at CSR position blk0: gathers + MMAs into acc
+  auto compute = [&](int nvalid, uint32_t mycol, int (&acc)[LC][RC][4]) {
     if (lane >= nvalid) mycol = 0u;
     if (lane < nvalid && mycol >= static_cast<uint32_t>(p.N)) {
       flag_status(p.status, MC_STATUS_BAD_INDEX);
@@ -126,7 +123,6 @@ sddmm_kernel(const SddmmParams p) {
     const uint32_t c_hi = __shfl_sync(0xffffffffu, mycol, g + 8);
     const bool lo_ok = g < nvalid, hi_ok = g + 8 < nvalid;
 
-    int acc[LC][RC][4];
 #pragma unroll
     for (int c = 0; c < LC; ++c)
 #pragma unroll
@@ -167,6 +163,8 @@ sddmm_kernel(const SddmmParams p) {
       }
     }
 
+  };
+  auto store = [&](int64_t blk0, int nvalid, const int (&acc)[LC][RC][4]) {
     // epilogue: D[m = block, n = v]; c0:(g,2t) c1:(g,2t+1) c2:(g+8,2t) c3:(g+8,2t+1)
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -194,6 +192,29 @@ sddmm_kernel(const SddmmParams p) {
         if (p.out_f16) p.out_f16[b * p.f16_stride + o] = f16_dequant(static_cast<int32_t>(total), alpha, alpha_f);
       }
     }
+  };
+
+  int64_t gi = gbeg;
+  // Speculative first group: with the uniform-row guess its column indices (spec_col) were
+  // loaded alongside the row offsets, so the B^T gathers start without waiting for them;
+  // the result is stored only if the real offsets confirm the guess (else recomputed).
+  const int64_t ge_g = (ng_g * (split + 1)) / p.splits;
+  if (gb_g < ge_g) {
+    const int nvalid_g = static_cast<int>(min_i64(16, hi_g - blk0_g));
+    int acc[LC][RC][4];
+    compute(nvalid_g, spec_col, acc);
+    if (spec_ok && gbeg == gb_g && gbeg < gend) {
+      store(blk0_g, nvalid_g, acc);
+      ++gi;
+    }
+  }
+  for (; gi < gend; ++gi) {
+    const int64_t blk0 = lo + gi * 16;
+    const int nvalid = static_cast<int>(min_i64(16, hi - blk0));
+    const uint32_t mycol = (lane < nvalid) ? __ldg(p.col_indices + blk0 + lane) : 0u;
+    int acc[LC][RC][4];
+    compute(nvalid, mycol, acc);
+    store(blk0, nvalid, acc);
   }
   if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
 }
