@@ -225,8 +225,12 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     int start = 0, end = 0;
     const int per_tile = static_cast<int>((static_cast<long long>(len_) * kCols + p.N - 1) / p.N);
     if (c0_ > 0) {
-      const int g = static_cast<int>((static_cast<double>(c0_) / static_cast<double>(p.N)) * len_);
-      const int margin = 64 + len_ / 16;
+      // interpolated position of c0; for columns sampled uniformly its spread is binomial
+      // (sigma = sqrt(len q (1 - q))), so +-(16 + 3 sigma) brackets it; rows that are not
+      // bracketed fall back to a binary search in global memory (correct, only slower)
+      const double q = static_cast<double>(c0_) / static_cast<double>(p.N);
+      const int g = static_cast<int>(q * len_);
+      const int margin = 16 + static_cast<int>(3.0 * sqrt(static_cast<double>(len_) * q * (1.0 - q)));
       start = g - margin > 0 ? g - margin : 0;
       end = g + margin;
     }
@@ -256,8 +260,12 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     tc::fence_barrier_init();
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
+    MC_STAMP(true, 100);
   }
-  if (warp == 1) tc::tmem_alloc<512>(smem_u32(tmem_holder));
+  if (warp == 1) {
+    tc::tmem_alloc<512>(smem_u32(tmem_holder));
+    MC_STAMP(lane == 0, 101);
+  }
   // everything above touches only this CTA's resources and the kernel parameters; inputs
   // written by a previous kernel are read only after pdl_wait
   if (threadIdx.x == 0) pdl_launch_dependents();
@@ -283,6 +291,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   }
   pdl_wait();
+  MC_STAMP(threadIdx.x == 0, 102);
   long long lo = 0, b_lo = 0, b_hi = 0, spec_lo = -1, spec_hi = -1;
   int len = 0, cur = 0, mtop = 0, landed = 0, lo511 = 0, lo63 = 0, depth = 2, c_first = 0;
   int mtop_last = 0;  // chunk bound of all cp.async groups but the most recent one
@@ -297,6 +306,8 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       b_hi = p.row_offsets[b_r + 1];
     }
   }
+  MC_STAMP(threadIdx.x == 0, 103);
+  MC_STAMP(threadIdx.x == 32 * kFirstBuild, 104);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();

@@ -38,7 +38,7 @@ buf = (ctypes.c_ulonglong * (148 * 128))()
 lib.mc_debug_timeline(buf, 148 * 128)
 t = np.frombuffer(buf, dtype=np.uint64).reshape(148, 128).astype(np.int64)
 base = t[:, 0].min()
-names = {0: "start", 1: "setup", 40: "search", 63: "end"}
+names = {0: "start", 1: "setup", 40: "search", 63: "end", 100: "binit", 101: "talloc", 102: "pdlw", 103: "prebar0", 104: "prebarB"}
 for i in range(6):
     names[2 + i] = f"tma{i}"
     names[10 + i] = f"mma_go{i}"
