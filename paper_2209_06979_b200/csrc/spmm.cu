@@ -33,7 +33,10 @@ namespace mcube {
 namespace {
 
 constexpr int kWarps = 4;
-constexpr int kStages = 4;
+#ifndef MCUBE_SPMM_KSTAGES
+#define MCUBE_SPMM_KSTAGES 3  // 3: twelve warps per SM at C5 (1.82 -> 1.63 ms); C3 neutral
+#endif
+constexpr int kStages = MCUBE_SPMM_KSTAGES;  // cp.async ring depth per warp
 constexpr int kSubN = 64;  // dense columns per MMA sub-tile (4 x m16 tiles)
 
 // A warp task covers NS sub-tiles of 64 columns: NS > 1 widens each gathered row
