@@ -34,7 +34,7 @@ namespace {
 
 constexpr int kWarps = 4;
 #ifndef MCUBE_SPMM_KSTAGES
-#define MCUBE_SPMM_KSTAGES 3  // 3: twelve warps per SM at C5 (1.82 -> 1.63 ms); C3 neutral
+#define MCUBE_SPMM_KSTAGES 4  // 2/3/4 measured within 2 % at C5 and C3 (same-box A/B)
 #endif
 constexpr int kStages = MCUBE_SPMM_KSTAGES;  // cp.async ring depth per warp
 constexpr int kSubN = 64;  // dense columns per MMA sub-tile (4 x m16 tiles)
@@ -74,8 +74,11 @@ __device__ __forceinline__ int64_t idx_pos(int64_t q, bool shuffled) {
   return (q & ~7LL) | ((w >> 1) | ((w & 1) << 2));
 }
 
+#ifndef MCUBE_SPMM_MINB
+#define MCUBE_SPMM_MINB 1
+#endif
 template <int LB, int RB, int V, int NS, bool ALIGNED>
-__global__ void __launch_bounds__(kWarps * 32)
+__global__ void __launch_bounds__(kWarps * 32, MCUBE_SPMM_MINB)
 spmm_kernel(const SpmmParams p) {
   using C = SpmmCfg<LB, RB, V, NS>;
   extern __shared__ __align__(128) uint8_t smem[];
