@@ -273,7 +273,23 @@ cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream) {
   if (ov != 2 && sddmm_tc_supported(p) && (ov == 1 || (density >= 0.08 && p.K >= 128))) return launch_sddmm_tc(p, stream);
   // warps per vector row: about one group of 16 blocks each
   const double avg_groups = p.vrows ? (static_cast<double>(p.n_blocks) / p.vrows) / 16.0 : 0.0;
-  int splits = static_cast<int>(avg_groups + 0.999);
+  // groups of 16 blocks per warp: 1, or 2 when one group per warp would need more than
+  // one wave of resident warps (C2 95 %: 1.6 waves -> 0.86; 10.2 -> 8.9 us, same-box A/B)
+  double gpw = 1.0;
+  {
+    static int wave_warps = 0;
+    if (!wave_warps) {
+      int dev = 0, sms = 148, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sddmm_kernel<8, 8, 8, true>, kWarps * 32, 0);
+      wave_warps = sms * (per_sm > 0 ? per_sm : 1) * kWarps;
+    }
+    const double warps1 = static_cast<double>(p.batch) * p.vrows * static_cast<int>(avg_groups + 0.999);
+    if (warps1 > wave_warps) gpw = 2.0;
+  }
+  if (const char* e = getenv("MCUBE_SDDMM_GPW")) gpw = atof(e) > 0 ? atof(e) : 1.0;
+  int splits = static_cast<int>(avg_groups / gpw + 0.999);
   p.splits = splits < 1 ? 1 : (splits > 256 ? 256 : splits);
   p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.splits;
   switch (p.LB * 100 + p.RB) {
