@@ -3,8 +3,12 @@
 softmax(Q K^T (masked) / sqrt(d)) V with symmetric absmax quantization, an
 SDDMM with fused dequant, a float softmax with fused requant, and an SpMM with
 fused dequant -- all in libmcube (mc_sparse_attention). `mode="parity"`
-reproduces the reference's float64 rounding chain; `mode="fast"` runs the
-softmax in float32 (stated tolerance: max-abs 1e-3 on the fp16 output).
+reproduces the reference's float64 rounding chain; `mode="fast"` evaluates exp with
+the fp32 ex2 unit (the exp-sum as exact fp32 TwoSum pairs) while every rounding decision
+-- quantisation, fp16 dequant, probability fp16 and requant levels -- is still taken
+exactly as the float64 chain would for those exp values (fp32 brackets with a float64
+fallback); stated tolerance: max-abs 1e-3 on the fp16 output. For fp16 inputs with
+8-bit Q/K/V and d = 64 the whole layer is two kernels.
 """
 
 from __future__ import annotations
