@@ -505,3 +505,40 @@ def test_attention_long_sequence_streams_quant_slices(mode):
     ref = O.attention(qh, kh, vh, offs, cols, L, d, 8, 8)
     err = float(np.abs(out[0].double().cpu().numpy() - ref["output"]).max())
     assert err <= (0.0 if mode == "parity" else mc.attention.FAST_MODE_TOLERANCE), err
+
+
+@pytest.mark.parametrize("v", [4, 8])
+@pytest.mark.parametrize("shape", [(1024, 2048, 256), (768, 1000, 128)])
+def test_sddmm_dense_16_row_tiles(v, shape, monkeypatch):
+    """The tcgen05 SDDMM with 16-vector-row tiles (MCUBE_SDDMM_VR=16): UMMA N = 16 V, half
+    the builder warps active, irregular rows."""
+    m, n, k = shape
+    monkeypatch.setenv("MCUBE_SDDMM_PATH", "dense")
+    monkeypatch.setenv("MCUBE_SDDMM_VR", "16")
+    rng = np.random.default_rng(m + n + k + v + 16)
+    offs, cols = _irregular_pattern(m, n, v, m + v + 16)
+    a = rng.integers(-128, 128, size=(m, k))
+    b = rng.integers(-128, 128, size=(k, n))
+    pat = mc.BcrsMatrix(m, n, v, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * v), 8))
+    out = mc.sddmm(mc.SddmmProblem(mc.pack_dense(a, 8, ROW_MAJOR), mc.pack_dense(b, 8, COL_MAJOR), pat))
+    want = O.sddmm(a, b, offs, cols, v, 8, 8)
+    assert (np.asarray(out.values) == want).all()
+
+
+@pytest.mark.parametrize("gpw", ["2", "3"])
+@pytest.mark.parametrize("pair", [(8, 8), (16, 16), (4, 4)])
+def test_sddmm_gather_several_groups_per_warp(gpw, pair, monkeypatch):
+    """Gather SDDMM with 2-3 groups of 16 blocks per warp (MCUBE_SDDMM_GPW), irregular rows."""
+    lb, rb = pair
+    monkeypatch.setenv("MCUBE_SDDMM_PATH", "gather")
+    monkeypatch.setenv("MCUBE_SDDMM_GPW", gpw)
+    m, n, k, v = 512, 1536, 128, 8
+    rng = np.random.default_rng(lb * 100 + rb + int(gpw))
+    offs, cols = _irregular_pattern(m, n, v, 77 + int(gpw))
+    lim = min((1 << (lb - 1)) - 1, 1000), min((1 << (rb - 1)) - 1, 1000)  # no int32 overflow at K=128
+    a = rng.integers(-lim[0], lim[0] + 1, size=(m, k))
+    b = rng.integers(-lim[1], lim[1] + 1, size=(k, n))
+    pat = mc.BcrsMatrix(m, n, v, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * v), 8))
+    out = mc.sddmm(mc.SddmmProblem(mc.pack_dense(a, lb, ROW_MAJOR), mc.pack_dense(b, rb, COL_MAJOR), pat))
+    want = O.sddmm(a, b, offs, cols, v, lb, rb)
+    assert (np.asarray(out.values) == want).all()
