@@ -396,7 +396,7 @@ def run_ours(args):
                    "parallelism": f"independent C2 sweep per rank x{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
                      "frac": achieved / peak_hbm, "traffic": load_traffic("sddmm_c2_s0.50"),
-                     "kernel": "sddmm_tc_kernel<8> (tcgen05 kind::i8) @ sparsity 0.50",
+                     "kernel": "sddmm_tc_kernel<8, 32> (tcgen05 kind::i8) @ sparsity 0.50",
                      "algorithmic_bytes": probs[dom]["bytes"], "peak_kind": peak_kind},
         "sweep": sweep,
         "e2e": e2e,
