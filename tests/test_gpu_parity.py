@@ -542,3 +542,25 @@ def test_sddmm_gather_several_groups_per_warp(gpw, pair, monkeypatch):
     out = mc.sddmm(mc.SddmmProblem(mc.pack_dense(a, lb, ROW_MAJOR), mc.pack_dense(b, rb, COL_MAJOR), pat))
     want = O.sddmm(a, b, offs, cols, v, lb, rb)
     assert (np.asarray(out.values) == want).all()
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+@pytest.mark.parametrize("bits", [(16, 8), (8, 4)])
+def test_attention_runner_other_precisions(mode, bits, monkeypatch):
+    """AttentionRunner on fp16 device inputs for (sb, qb) = (16, 8) (fused scores/softmax with
+    16-bit SR-BCRS probabilities + L16-R8 SpMM) and (8, 4) (unfused 4-bit pipeline), vs oracle."""
+    import torch
+    sb, qb = bits
+    L, d, heads, sp = 512, 64, 2, 0.9
+    a = O.build_attention_case(L, d, sp, seed=sb * 10 + qb)
+    offs, cols = a["offsets"], a["col_indices"]
+    mask = mc.BcrsMatrix(L, L, 8, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * 8), 8))
+    cfg = mc.AttentionConfig(L, sb, qb, mask, head_dim=d, num_heads=heads)
+    g = torch.Generator(device="cuda").manual_seed(sb + qb)
+    q, k, v = (torch.randn((heads, L, d), device="cuda", generator=g).half() for _ in range(3))
+    out = mc.AttentionRunner(cfg, heads, mode=mode)(q, k, v, check=True).clone()
+    for h in range(heads):
+        qh, kh, vh = (x[h].double().cpu().numpy() for x in (q, k, v))
+        ref = O.attention(qh, kh, vh, offs, cols, L, d, sb, qb)
+        err = float(np.abs(out[h].double().cpu().numpy() - ref["output"]).max())
+        assert err <= (0.0 if mode == "parity" else mc.attention.FAST_MODE_TOLERANCE), (h, err)
