@@ -564,3 +564,33 @@ def test_attention_runner_other_precisions(mode, bits, monkeypatch):
         ref = O.attention(qh, kh, vh, offs, cols, L, d, sb, qb)
         err = float(np.abs(out[h].double().cpu().numpy() - ref["output"]).max())
         assert err <= (0.0 if mode == "parity" else mc.attention.FAST_MODE_TOLERANCE), (h, err)
+
+
+@pytest.mark.parametrize("mode", ["parity", "fast"])
+def test_attention_fused_irregular_mask_rows(mode):
+    """The two-kernel C4 path on a mask whose vector rows hold 0, 1, ..., 480 (the fused
+    kernel's cache), 481 and up to all 2048 blocks: empty rows give 0, long rows recompute."""
+    import torch
+    L, d, heads = 2048, 64, 2
+    rng = np.random.default_rng(2048)
+    lens = [0, 1, 5, 31, 32, 33, 100, 479, 480, 481, 1000, 2048]
+    offs, cols = [0], []
+    for r in range(L // 8):
+        n = lens[r % len(lens)]
+        c = np.sort(rng.choice(L, size=n, replace=False)).astype(np.uint32)
+        cols.append(c)
+        offs.append(offs[-1] + n)
+    offs = np.array(offs, dtype=np.int64)
+    cols = np.concatenate(cols)
+    mask = mc.BcrsMatrix(L, L, 8, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * 8), 8))
+    cfg = mc.AttentionConfig(L, 8, 8, mask, head_dim=d, num_heads=heads)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = (torch.randn((heads, L, d), device="cuda", generator=g).half() for _ in range(3))
+    out = mc.AttentionRunner(cfg, heads, mode=mode)(q, k, v, check=True).clone()
+    for h in range(heads):
+        qh, kh, vh = (x[h].double().cpu().numpy() for x in (q, k, v))
+        ref = O.attention(qh, kh, vh, offs, cols, L, d, 8, 8)
+        got = out[h].double().cpu().numpy()
+        assert (got[:8] == 0).all()  # vector row 0 is empty
+        err = float(np.abs(got - ref["output"]).max())
+        assert err <= (0.0 if mode == "parity" else mc.attention.FAST_MODE_TOLERANCE), (h, err)
