@@ -148,8 +148,11 @@ int mc_sddmm_batched(const mc_dense* a, int64_t a_words_stride,
  *   mc_srbcrs_plan: row_begin/row_end from row_offsets and the stride,
  *                   total stored vectors into *stored_total (device int64);
  *   mc_srbcrs_fill: sentinel-padded col_indices and the strided values.
- * `values` are `bits`-bit packed words (4/8/12/16) or raw 32-bit elements
- * (bits == 32: int32 accumulators / float32 epilogue outputs).
+ * `values` are `bits`-bit packed words (4/8/12/16), raw 32-bit elements
+ * (bits == 32: int32 accumulators / float32 epilogue outputs) or raw 64-bit
+ * elements (bits == 64: int64 / float64 epilogue outputs). Raw 16-bit
+ * elements (float16 / int16) are moved as bits == 16 words. The element type
+ * is kept, as the reference's values.astype(b.values.dtype) does.
  * ------------------------------------------------------------------- */
 int mc_srbcrs_plan(const mc_bcrs* pattern, int32_t stride, int64_t* row_begin,
                    int64_t* row_end, int64_t* stored_total, void* stream);

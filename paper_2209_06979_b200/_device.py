@@ -40,7 +40,22 @@ def to_dev(x, np_dtype, device=None):
     return tt.to(dev, non_blocking=True).contiguous()
 
 
+def _freeze(obj):
+    """Make the container's host arrays read-only once a device copy of them is cached:
+    the containers are immutable by contract (frozen dataclasses, as in the reference),
+    and an in-place edit would otherwise leave the cached device copy stale."""
+    for name in ("row_begin", "row_end", "row_offsets", "col_indices", "words", "values"):
+        x = obj.__dict__.get(name)
+        x = getattr(x, "words", x)
+        if isinstance(x, np.ndarray) and x.flags.writeable:
+            try:
+                x.flags.writeable = False
+            except ValueError:
+                pass
+
+
 def cached(obj, key, make):
+    _freeze(obj)
     cache = obj.__dict__.get("_dev_cache")
     if cache is None:
         cache = {}
@@ -118,6 +133,13 @@ def status_word():
     if dev not in _status:
         _status[dev] = t.zeros(1, dtype=t.int32, device=f"cuda:{dev}")
     return _status[dev]
+
+
+def fresh_status():
+    """A zeroed status word for one checked launch: flags left by unchecked launches
+    (status_word) or by launches on other streams never reach a checked call."""
+    t = torch()
+    return t.zeros(1, dtype=t.int32, device=f"cuda:{t.cuda.current_device()}")
 
 
 def fetch_status(status, stream=None):

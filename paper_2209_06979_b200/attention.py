@@ -160,7 +160,7 @@ class AttentionRunner:
                 raise ValueError(f"Q, K, V must be {expect[1:]} per head, batch {self.batch}")
         a = self.args
         a.q, a.k, a.v, a.in_dtype = N.ptr(qd), N.ptr(kd), N.ptr(vd), dt
-        status = D.status_word()
+        status = D.fresh_status() if check else D.status_word()
         N.check(N.lib().mc_sparse_attention(N.ctypes.byref(a), N.ptr(status), N.stream_ptr(stream)))
         if check:
             D.fetch_status(status, stream)

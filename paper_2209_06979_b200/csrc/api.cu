@@ -252,8 +252,8 @@ int mc_srbcrs_fill(const mc_bcrs* pattern, int32_t stride, const int64_t* row_be
                    int64_t stored_total, const uint32_t* values, int32_t bits, uint32_t* col_out,
                    uint32_t* values_out, void* stream) {
   if (!pattern) return fail(MC_ERR_VALUE, "null pattern");
-  if (bits != 4 && bits != 8 && bits != 12 && bits != 16 && bits != 32)
-    return fail(MC_ERR_VALUE, "bits must be 4, 8, 12, 16 or 32");
+  if (bits != 4 && bits != 8 && bits != 12 && bits != 16 && bits != 32 && bits != 64)
+    return fail(MC_ERR_VALUE, "bits must be 4, 8, 12, 16, 32 or 64");
   const int64_t vrows = pattern->scalar_rows / pattern->vector_length;
   return cuda_status(launch_srbcrs_fill(pattern->row_offsets, pattern->col_indices, vrows, pattern->n_blocks,
                                         pattern->vector_length, stride, row_begin, row_end, stored_total, values, bits,

@@ -186,6 +186,16 @@ cudaError_t launch_densify_l(const SpmmParams& p, int8_t* a0, int8_t* a1, cudaSt
 
 }  // namespace
 
+// densify_kernel stages a row's values in batches of whole strides; a stride wider than
+// one batch cannot be staged (the batch loop would not advance), so such problems take
+// the gather kernels.
+bool densify_stride_ok(const SpmmParams& p) {
+  if (p.S <= 0 || p.V <= 0 || p.LB <= 0) return false;
+  int64_t per_batch = (static_cast<int64_t>(kVB) * 32 - 32) / (static_cast<int64_t>(p.V) * p.LB);
+  if (per_batch > 8 * 256) per_batch = 8 * 256;  // kQ positions per thread x 256 threads
+  return per_batch / p.S * p.S >= p.S;
+}
+
 int dense_lhs_planes(int lb) { return lb >= 12 ? 2 : 1; }
 int dense_rhs_planes(int rb) { return rb == 16 ? 2 : 1; }
 

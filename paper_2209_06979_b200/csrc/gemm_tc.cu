@@ -302,6 +302,9 @@ bool dense_spmm_eligible(const SpmmParams& p) {
   if (p.batch != 1 || p.out == nullptr || p.out_f16 != nullptr) return false;
   if (p.M % kTM || p.N % 128 || p.K % kKB || p.M <= 0 || p.N <= 0 || p.K <= 0) return false;
   if (p.stored <= 0 || encode_fn() == nullptr) return false;
+  // byte-chunk planes only: nibble-chunk plans and strides wider than a staging batch take
+  // the gather kernels
+  if (spmm_needs_nibble_chunks(p) || !densify_stride_ok(p)) return false;
   if ((reinterpret_cast<uintptr_t>(p.rhs_words) & 15) || (reinterpret_cast<uintptr_t>(p.out) & 15)) return false;
   const double density = static_cast<double>(p.stored) * p.V / (static_cast<double>(p.M) * p.K);
   const char* e = getenv("MCUBE_SPMM_PATH");

@@ -69,6 +69,10 @@ struct SddmmTcParams {
 };
 
 cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream);
+// true when a 4-bit-width plan must keep the reference's per-nibble chunk accumulators
+bool spmm_needs_nibble_chunks(const SpmmParams& p);
+// the densify kernel's value staging can hold whole strides of this problem
+bool densify_stride_ok(const SpmmParams& p);
 // dense-tile path for moderate sparsity (dense.cu + gemm_tc.cu): densify the LHS into int8
 // planes in a caller-provided workspace, then an exact tcgen05 GEMM
 bool dense_spmm_eligible(const SpmmParams& p);

@@ -106,6 +106,23 @@ __global__ void srbcrs_fill_val_kernel(const int64_t* __restrict__ offs, int64_t
   dst[w] = static_cast<uint32_t>(acc);
 }
 
+// raw 64-bit values (float64 / int64 block values, e.g. dequantised SDDMM outputs): one
+// thread per output element, zero for padding slots (sparse_format.py:303-304 keeps dtype)
+__global__ void srbcrs_fill_val64_kernel(const int64_t* __restrict__ offs, int64_t vrows, int V, int S,
+                                         const int64_t* __restrict__ begin, const int64_t* __restrict__ end,
+                                         int64_t n_elems, const uint2* __restrict__ src, uint2* __restrict__ dst) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n_elems) return;
+  const int64_t vs = static_cast<int64_t>(V) * S;
+  const int64_t s = e / vs;
+  const int64_t within = e - s * vs;
+  const int64_t v = within / S;
+  const int64_t pst = s * S + (within - v * S);
+  const int64_t r = upper_row(begin, vrows, pst);
+  const int64_t j = pst - begin[r];
+  dst[e] = (j < end[r] - begin[r]) ? src[(offs[r] + j) * V + v] : make_uint2(0u, 0u);
+}
+
 __global__ void shuffle_kernel(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ out) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
@@ -135,7 +152,14 @@ cudaError_t launch_srbcrs_fill(const int64_t* row_offsets, const uint32_t* col_i
                                                      stored_total, col_out);
     count_launch();
   }
-  if (values_out) {
+  if (values_out && bits == 64) {
+    const int64_t n_elems = stored_total * V;
+    const unsigned grid = static_cast<unsigned>((n_elems + 255) / 256);
+    srbcrs_fill_val64_kernel<<<grid, 256, 0, stream>>>(row_offsets, vrows, V, stride, row_begin, row_end, n_elems,
+                                                       reinterpret_cast<const uint2*>(values),
+                                                       reinterpret_cast<uint2*>(values_out));
+    count_launch();
+  } else if (values_out) {
     const int64_t n_elems = stored_total * V;
     const int64_t n_words = (n_elems * bits + 31) / 32;
     const unsigned grid = static_cast<unsigned>((n_words + 255) / 256);

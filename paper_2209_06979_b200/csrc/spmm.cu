@@ -41,9 +41,14 @@ constexpr int kSubN = 64;  // dense columns per MMA sub-tile (4 x m16 tiles)
 
 // A warp task covers NS sub-tiles of 64 columns: NS > 1 widens each gathered row
 // segment to 128 bytes (one L2 line) for 4- and 8-bit RHS at large N.
-template <int LB, int RB, int V, int NS>
+// NIB: the reference's 4-bit-width plan chunks (emulation.py:80-83) -- one LHS chunk per
+// nibble (lower nibbles u8, the top one s8) instead of byte chunks. Used for RB = 4 with an
+// 8/12/16-bit LHS when K is large enough for one of the reference's per-nibble group checks
+// (tile_engine.py:246-247 via kernels.py:265-275) to fire, or for a byte-chunk int32
+// accumulator to wrap (spmm_needs_nibble_chunks).
+template <int LB, int RB, int V, int NS, bool NIB = false>
 struct SpmmCfg {
-  static constexpr int LC = (LB >= 12) ? 2 : 1;        // LHS int8 chunks
+  static constexpr int LC = NIB ? LB / 4 : ((LB >= 12) ? 2 : 1);  // LHS int8 chunks
   static constexpr int RC = (RB == 16) ? 2 : 1;        // RHS int8 chunks
   static constexpr int TN = kSubN * NS;                // dense columns per task
   static constexpr int SUB = kSubN * RB / 8;           // bytes of one 64-column sub-segment
@@ -77,10 +82,11 @@ __device__ __forceinline__ int64_t idx_pos(int64_t q, bool shuffled) {
 #ifndef MCUBE_SPMM_MINB
 #define MCUBE_SPMM_MINB 1
 #endif
-template <int LB, int RB, int V, int NS, bool ALIGNED>
+template <int LB, int RB, int V, int NS, bool ALIGNED, bool NIB>
 __global__ void __launch_bounds__(kWarps * 32, MCUBE_SPMM_MINB)
 spmm_kernel(const SpmmParams p) {
-  using C = SpmmCfg<LB, RB, V, NS>;
+  using C = SpmmCfg<LB, RB, V, NS, NIB>;
+  static_assert(!NIB || (RB == 4 && LB >= 8), "nibble chunks are the 4-bit-width plans of an 8/12/16-bit LHS");
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -260,7 +266,7 @@ spmm_kernel(const SpmmParams p) {
     const uint8_t* sa = sb + C::B_STAGE;
 
     // ---- MMA B operand: LHS chunk words for kk = 16h + 4t .. +3 of row v = g ----
-    uint32_t bf[C::LC][2];
+    uint32_t bf[C::LC > 2 ? C::LC : 2][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint8_t* ar = sa + (h * V + (g < V ? g : 0)) * C::ABYTES;
@@ -281,6 +287,25 @@ spmm_kernel(const SpmmParams p) {
         // low byte (unsigned chunk), high nibble sign-extended (signed chunk)
         bf[0][h] = (e0 & 0xFF) | ((e1 & 0xFF) << 8) | ((e2 & 0xFF) << 16) | ((e3 & 0xFF) << 24);
         bf[1][h] = sext_nibble_bytes((e0 >> 8) | ((e1 >> 8) << 8) | ((e2 >> 8) << 16) | ((e3 >> 8) << 24));
+      }
+      if constexpr (NIB) {
+        // byte chunks -> nibble chunks (qint.py:209-225 at w = 4): lower nibbles unsigned,
+        // the top nibble signed
+        if constexpr (LB == 8) {
+          const uint32_t w = bf[0][h];
+          bf[0][h] = w & 0x0F0F0F0Fu;
+          bf[1][h] = sext_nibble_bytes((w >> 4) & 0x0F0F0F0Fu);
+        } else {
+          const uint32_t lo = bf[0][h], hi = bf[1][h];  // u8 low byte, s8 high part
+          bf[0][h] = lo & 0x0F0F0F0Fu;
+          bf[1][h] = (lo >> 4) & 0x0F0F0F0Fu;
+          if constexpr (LB == 16) {
+            bf[2][h] = hi & 0x0F0F0F0Fu;
+            bf[3][h] = sext_nibble_bytes((hi >> 4) & 0x0F0F0F0Fu);
+          } else {
+            bf[2][h] = hi;  // 12-bit: the high part already is the signed top nibble
+          }
+        }
       }
       if (g >= V) {
 #pragma unroll
@@ -352,7 +377,7 @@ spmm_kernel(const SpmmParams p) {
 #pragma unroll
         for (int c = 0; c < C::LC; ++c) {
           const bool au = (RB == 16) && (j == 0);
-          const bool bu = (LB >= 12) && (c == 0);
+          const bool bu = NIB ? (c < C::LC - 1) : ((LB >= 12) && (c == 0));
           if (au && bu) mma16832<true, true>(acc[st][c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
           else if (au) mma16832<true, false>(acc[st][c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
           else if (bu) mma16832<false, true>(acc[st][c][j][q], a0, a1, a2, a3, bf[c][0], bf[c][1]);
@@ -382,7 +407,22 @@ spmm_kernel(const SpmmParams p) {
 #pragma unroll
       for (int j = 0; j < C::RC; ++j) {
         long long tj;
-        if constexpr (C::LC == 2) {
+        if constexpr (NIB) {
+          // the reference's stacking groups at w = 4 (kernels.py:121-128): V = 8 one chunk per
+          // group, V = 4 pairs, V = 2 quads; each weighted group sum must fit int32
+          // (tile_engine.py:246-247)
+          constexpr int per = V < 8 ? 8 / V : 1;
+          tj = 0;
+#pragma unroll
+          for (int g0 = 0; g0 < C::LC; g0 += per) {
+            long long comb = 0;
+#pragma unroll
+            for (int c = g0; c < g0 + per && c < C::LC; ++c)
+              comb += static_cast<long long>(acc[st][c][j][q][e]) << (4 * c);
+            overflow |= !fits_i32(comb);
+            tj += comb;
+          }
+        } else if constexpr (C::LC == 2) {
           const long long lo = acc[st][0][j][q][e];
           const long long hi = 256LL * acc[st][1][j][q][e];
           constexpr bool w8 = (RB != 4);
@@ -436,9 +476,9 @@ spmm_kernel(const SpmmParams p) {
   if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
 }
 
-template <int LB, int RB, int V, int NS>
+template <int LB, int RB, int V, int NS, bool NIB = false>
 cudaError_t launch_spmm_v(SpmmParams p, cudaStream_t stream) {
-  using C = SpmmCfg<LB, RB, V, NS>;
+  using C = SpmmCfg<LB, RB, V, NS, NIB>;
   p.ntiles = (p.N + C::TN - 1) / C::TN;
   p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.ntiles;
   const int smem = kWarps * kStages * C::STAGE + kWarps * 2048;  // + per-warp index ring
@@ -447,11 +487,11 @@ cudaError_t launch_spmm_v(SpmmParams p, cudaStream_t stream) {
   const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
   if (grid == 0) return cudaSuccess;
   if (aligned) {
-    auto k = spmm_kernel<LB, RB, V, NS, true>;
+    auto k = spmm_kernel<LB, RB, V, NS, true, NIB>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (const cudaError_t e = launch_pdl(k, dim3(grid), dim3(kWarps * 32), smem, stream, p)) return e;
   } else {
-    auto k = spmm_kernel<LB, RB, V, NS, false>;
+    auto k = spmm_kernel<LB, RB, V, NS, false, NIB>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (const cudaError_t e = launch_pdl(k, dim3(grid), dim3(kWarps * 32), smem, stream, p)) return e;
   }
@@ -476,6 +516,15 @@ cudaError_t launch_spmm_ns(const SpmmParams& p, cudaStream_t stream) {
 
 template <int LB, int RB>
 cudaError_t launch_spmm_lr(const SpmmParams& p, cudaStream_t stream) {
+  if constexpr (RB == 4 && LB >= 8) {
+    if (spmm_needs_nibble_chunks(p)) {
+      switch (p.V) {
+        case 2: return launch_spmm_v<LB, RB, 2, 1, true>(p, stream);
+        case 4: return launch_spmm_v<LB, RB, 4, 1, true>(p, stream);
+        default: return launch_spmm_v<LB, RB, 8, 1, true>(p, stream);
+      }
+    }
+  }
   switch (p.V) {
     case 2: return launch_spmm_ns<LB, RB, 2>(p, stream);
     case 4: return launch_spmm_ns<LB, RB, 4>(p, stream);
@@ -484,6 +533,28 @@ cudaError_t launch_spmm_lr(const SpmmParams& p, cudaStream_t stream) {
 }
 
 }  // namespace
+
+// 4-bit-width plans with an 8/12/16-bit LHS (emulation.py:80-83) run as int8 byte-chunk
+// products unless K (which bounds every row's stored vectors, rounded up to the stride) is
+// large enough that (a) a byte-chunk int32 accumulator could wrap, or (b) at V = 8 one of
+// the reference's per-nibble group checks |2^(4c) * sum_k chunk_c(a) * b| <= INT32_MAX
+// (tile_engine.py:246-247) could fail while the final result still fits. Then the kernel
+// keeps one accumulator per nibble chunk, as the reference does, and evaluates every check.
+bool spmm_needs_nibble_chunks(const SpmmParams& p) {
+  if (p.RB != 4 || p.LB < 8) return false;
+  const long double sb = static_cast<long double>(((p.K + p.S - 1) / p.S) * p.S);
+  const long double lim = 2147483647.0L;
+  // byte chunks x s4: s8 * s4 <= 128 * 8; u8 * s4 <= 255 * 8
+  const long double byte_term = p.LB == 8 ? 1024.0L : 2040.0L;
+  if (sb * byte_term > lim) return true;
+  if (p.V != 8) return false;  // V = 4 / 2 group sums are byte-chunk (or final) sums: exact
+  const int nch = p.LB / 4;
+  for (int c = 1; c < nch; ++c) {  // chunk 0: |sum| <= K * 120, bounded by the K check
+    const long double term = (c == nch - 1 ? 64.0L : 120.0L) * static_cast<long double>(1LL << (4 * c));
+    if (sb * term > lim) return true;
+  }
+  return false;
+}
 
 cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream) {
   if (spmm_tc_supported(p)) return launch_spmm_tc(p, stream);

@@ -125,7 +125,7 @@ def spmm_device(p: SpmmProblem, out=None, stream=None, check_status: bool = True
     rhs, _k2 = D.dense_struct(p.rhs)
     if out is None:
         out = t.empty((p.lhs.scalar_rows, p.rhs.cols), dtype=t.int32, device="cuda")
-    status = D.status_word()
+    status = D.fresh_status() if check_status else D.status_word()
     s = N.stream_ptr(stream)
     # moderate sparsity: the library densifies the LHS into a workspace and runs an exact
     # tcgen05 GEMM (mc_spmm_workspace reports 0 when the gather kernels are used)
@@ -198,7 +198,7 @@ def sddmm_device(p: SddmmProblem, out=None, stream=None, check_status: bool = Tr
     v = p.out_pattern.vector_length
     if out is None:
         out = t.empty(p.out_pattern.n_blocks * v, dtype=t.int32, device="cuda")
-    status = D.status_word()
+    status = D.fresh_status() if check_status else D.status_word()
     s = N.stream_ptr(stream)
     N.check(lib.mc_sddmm(a, b, pat, N.ptr(out), N.ptr(status), s))
     if check_status:

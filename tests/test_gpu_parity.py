@@ -107,6 +107,28 @@ def test_device_packer_and_shuffle(case):
             mc.shuffle_indices(sh)
 
 
+@pytest.mark.parametrize("dtype", ["float64", "int64", "float32", "int32", "float16", "int16"])
+@pytest.mark.parametrize("where", ["host", "device"])
+def test_device_packer_keeps_raw_value_dtype(dtype, where):
+    """Raw (unpacked) block values keep their dtype through the device packer, like the
+    reference's values.astype(b.values.dtype) (sparse_format.py:303-304)."""
+    offs, cols, _ = O.synthetic_bcrs(64, 96, 4, 0.8, 11, 8)
+    rng = np.random.default_rng(5)
+    vals = (rng.normal(size=cols.size * 4) * 1000).astype(dtype)
+    b_host = mc.BcrsMatrix(64, 96, 4, offs, cols, vals)
+    want_b, want_e, want_i, want_v = O.srbcrs_from_bcrs(offs, cols, vals, 4, 16)
+    if where == "device":
+        b = mc.BcrsMatrix(64, 96, 4, torch.from_numpy(offs).cuda(),
+                          torch.from_numpy(cols.view(np.int32)).cuda(), torch.from_numpy(vals).cuda())
+        s = mc.bcrs_to_srbcrs(b, 16)
+        got = s.values.cpu().numpy()
+    else:
+        s = mc.bcrs_to_srbcrs(b_host, 16)
+        got = np.asarray(s.values)
+    assert got.dtype == np.dtype(dtype)
+    assert (got.view(np.uint8) == want_v.astype(dtype).view(np.uint8)).all()
+
+
 def test_packer_hand_layout_and_generator():
     d = FMT["hand_dense"]
     s = mc.bcrs_to_srbcrs(mc.dense_to_bcrs(d, 2), 4)

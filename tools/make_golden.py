@@ -118,8 +118,78 @@ def attention_case(d, name, seq_len, sb, qb, sparsity, seed, head_dim=64, dense_
                                 res.params["v"].scale, res.params["softmax"].scale])
 
 
+def irregular_csr(rows, cols, seed):
+    """An irregular DLMC-like pattern: per-row lengths 0..cols/3, sorted distinct columns."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, cols // 3 + 1, rows)
+    lens[::7] = 0  # empty rows
+    lens[3] = cols  # one full row
+    idx = [np.sort(rng.choice(cols, size=int(n), replace=False)) for n in lens]
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    return sf.CsrMatrix(rows, cols, int(offs[-1]), offs, np.concatenate(idx).astype(np.uint32))
+
+
+def extra_goldens():
+    """Round-2 fixtures: DLMC ingestion through the reference bench builders
+    (bench.py:93-126, sparse_format.py:388-450) and the reference's per-nibble group
+    check of 4-bit-width plans (tile_engine.py:246-247 via kernels.py:265-275)."""
+    import io
+    d = {}
+    tiny = "3, 5, 2\n0 1 1 2\n4 0\n"  # test_sparse_format.py:10
+    csr = sf.read_dlmc(tiny)
+    d["dlmc_tiny/text"] = np.frombuffer(tiny.encode(), dtype=np.uint8)
+    d["dlmc_tiny/offsets"] = csr.row_offsets
+    d["dlmc_tiny/cols"] = csr.col_indices
+    csr = irregular_csr(48, 256, seed=21)
+    buf = io.StringIO()
+    sf.write_dlmc(csr, buf)
+    text = buf.getvalue()
+    d["dlmc_irr/text"] = np.frombuffer(text.encode(), dtype=np.uint8)
+    for (lb, rbits, v) in [(8, 8, 8), (8, 4, 8), (16, 8, 4), (4, 4, 2), (16, 16, 8)]:
+        spec = rb.SweepSpec("spmm", [(0, 64, 256)], dlmc=sf.read_dlmc(text))
+        seed = 1000 + lb * 10 + rbits + v
+        prob, (m, n, k), _, _ = rb._build_spmm(spec, (0, 64, 256), v, 0.0, lb, rbits, seed)
+        out = kn.spmm(prob)
+        p = f"dlmc_spmm_{lb}_{rbits}_v{v}/"
+        d[p + "args"] = np.array([m, n, k, v, lb, rbits, seed], dtype=np.int64)
+        srbcrs_arrays(p + "lhs_", prob.lhs, d)
+        d[p + "rhs_words"] = prob.rhs.words
+        d[p + "out"] = out
+    for (lb, rbits, v) in [(8, 8, 8), (16, 16, 4), (4, 4, 8)]:
+        spec = rb.SweepSpec("sddmm", [(0, 0, 96)], dlmc=sf.read_dlmc(text))
+        seed = 2000 + lb * 10 + rbits + v
+        prob, (m, n, k), _, _ = rb._build_sddmm(spec, (0, 0, 96), v, 0.0, lb, rbits, seed)
+        out = kn.sddmm(prob)
+        p = f"dlmc_sddmm_{lb}_{rbits}_v{v}/"
+        d[p + "args"] = np.array([m, n, k, v, lb, rbits, seed], dtype=np.int64)
+        d[p + "offsets"] = prob.out_pattern.row_offsets
+        d[p + "cols"] = prob.out_pattern.col_indices
+        d[p + "a_words"] = prob.a.words
+        d[p + "b_words"] = prob.b.words
+        d[p + "out"] = np.asarray(out.values)
+    # per-nibble group check (L16-R4, V = 8): the top-nibble group sum 4096 * sum(c3 * b)
+    # leaves int32 while the final result still fits -> the reference raises
+    for name, aval, k in [("nib_raise", -28673, 9216), ("nib_ok", 100, 9216)]:
+        dense = np.full((8, k), aval, dtype=np.int64)
+        lhs = sf.shuffle_indices(sf.bcrs_to_srbcrs(sf.dense_to_bcrs(dense, 8, bit_width=16), 32))
+        rhs = qint.pack_dense(np.full((k, 64), -8, dtype=np.int64), 4)
+        p = name + "/"
+        d[p + "args"] = np.array([aval, k], dtype=np.int64)
+        try:
+            d[p + "out"] = kn.spmm(kn.SpmmProblem(lhs, rhs))
+            d[p + "raises"] = np.array([0])
+        except Exception as e:  # OverflowRiskError
+            d[p + "raises"] = np.array([1])
+            d[p + "error"] = np.frombuffer(type(e).__name__.encode(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(OUT, "extra.npz"), **d)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if os.environ.get("GOLDEN_ONLY") == "extra":
+        extra_goldens()
+        return
+    extra_goldens()
 
     # ---- qint / sparse_format KATs ----
     d = {}
