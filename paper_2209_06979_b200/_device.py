@@ -7,6 +7,8 @@ with the same sparse matrix pay the host-to-device copy once.
 
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 
 from . import _native as N
@@ -35,7 +37,9 @@ def to_dev(x, np_dtype, device=None):
         view = {np.uint32: np.int32, np.uint64: np.int64}.get(np.dtype(np_dtype).type, None)
         if view is not None:
             arr = arr.view(view)
-        tt = t.from_numpy(arr)
+        with warnings.catch_warnings():  # read-only (frozen) host arrays: copied to the device below
+            warnings.simplefilter("ignore", UserWarning)
+            tt = t.from_numpy(arr)
     dev = device if device is not None else t.device("cuda", t.cuda.current_device())
     return tt.to(dev, non_blocking=True).contiguous()
 
