@@ -1,21 +1,33 @@
 """Benchmark for the Magicube B200 hot path (driver contract: one JSON line on rank 0).
 
-Headline workload (BASELINE.json configs[1], "C2"): SDDMM L8-R8, V=8,
-M=N=4096, K=256 over the sparsity sweep 50/70/90/95/98%. One step = one
-SDDMM launch per sparsity (5 launches) on inputs resident in HBM. The C2
-operands fit in L2, so every problem has several device copies and consecutive
-steps rotate through them (> 320 MiB per rotation): no launch finds its inputs
-in L2, and no flush kernel sits between timed launches. metric = TOPS = sum(2*V*K*nblk) / device time. Multi-GPU: one process per
-GPU, each rank runs its own C2 sweep (independent problems, weak scaling, no
-collective in the timed region); time = max over ranks.
+BASELINE.json metric: "SpMM/SDDMM TOPS vs sparsity & precision pair; sparse-attn seq/s at
+1/2/4/8 B200". One line carries every config:
 
-`e2e` times the same sweep through the C-ABI entry point mc_sddmm with pinned
-host buffers: every step copies A, B^T and the patterns host->device and the
-int32 block values device->host inside the timed region.
+* headline `value` -- C2 (configs[1]): SDDMM L8-R8, V=8, M=N=4096, K=256 over the sparsity
+  sweep 50/70/90/95/98 %. One step = one SDDMM launch per sparsity (5 launches) on inputs
+  resident in HBM. The C2 operands fit in L2, so every problem has several device copies and
+  consecutive steps rotate through them (> 320 MiB per rotation): no launch finds its inputs
+  in L2. TOPS = sum(2*V*K*nblk) / device time. At N > 1 the sweep is ONE problem per sparsity
+  of M = 4096*N rows, split into N vector-row panels (weak scaling: every rank
+  owns a 4096-row panel, the same work as N = 1), time = max over ranks.
+* `c3` -- SpMM precision x V x sparsity grid at M=K=4096, N=512 (5 pairs x {2,4,8} x
+  {70,90,98} %), each cell split into N row panels (strong), L2 flushed before every launch;
+* `c4` -- fused 8-bit sparse attention, B=64 x H=8 heads, L=4096, d=64, 90 % mask; the 512
+  (batch, head) pairs split over the N ranks (strong); seq/s = 64 / layer time;
+* `c5` -- SpMM L8-R4, M=K=32768, N=2048, 95 %, split into N row panels (strong).
 
-`--impl reference` times the reference algorithm's CPU implementation (the
-oracle port, oracle/magicube_ref.py -- the reference itself is pure Python and
-cannot travel to the GPU box) on the same workload and metric.
+Every result is checked against the CPU oracle on sampled rows / heads before timing (plus
+an NCCL all-gather of the per-rank verdicts and checksums, outside every timed region).
+`e2e` times the C2 sweep through the C-ABI entry point mc_sddmm with pinned host buffers:
+every step copies A, B^T and the patterns host->device and the int32 block values
+device->host inside the timed region.
+
+`--impl reference` times the reference's own CPU implementation (qsparse.kernels.sddmm from
+baseline/_ref, installed from /root/reference; the oracle port when it is absent) on the same
+C2 workload and metric: each step is a bounded row sample of every C2 problem spread over all
+host cores (one process per core), with a 1-core figure beside it.
+`--inject-fault` flips one device output element before validation (the reference bench's
+negative control, bench.py:151-190): the line reports whether validation caught it.
 """
 
 from __future__ import annotations
@@ -40,6 +52,12 @@ V = 8
 BITS = 8
 COLD_BYTES = 320 << 20  # bytes touched per input rotation (> 2x the 126 MB L2)
 METRIC = "SpMM/SDDMM TOPS vs sparsity & precision pair; sparse-attn seq/s at 1/2/4/8 B200"
+C2_WORKLOAD = "C2 SDDMM L8-R8 V=8 M=N=4096 K=256 sparsity 50/70/90/95/98%"
+C3_PAIRS = ((16, 16), (16, 8), (8, 8), (8, 4), (4, 4))
+C3_SPARSITIES = (0.7, 0.9, 0.98)
+C4 = dict(batch=64, heads=8, seq=4096, d=64, sparsity=0.9)
+C5 = dict(m=32768, k=32768, n=2048, v=8, sparsity=0.95, lb=8, rb=4)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
 
 def dist_info():
@@ -58,13 +76,29 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def build_c2(seed_base: int):
-    """C2 inputs with the reference generators (bench.py:113-126 semantics)."""
+# ---------------------------------------------------------------------------------------
+# problem construction (reference generators, oracle.build_* = bench._build_* semantics)
+# ---------------------------------------------------------------------------------------
+
+def c2_rank_cases(rank: int, world: int):
+    """This rank's vector-row panel of every C2 problem.
+
+    The global problem per sparsity has M = 4096 * world rows (the reference generator with
+    the reference cell seed of that shape); rank r owns vector rows [512 r, 512 (r + 1)),
+    i.e. exactly the N = 1 problem's work. world = 1 gives the C2 problems themselves.
+    """
     import oracle as O
     cases = []
+    mg = M * world
     for s in SPARSITIES:
-        seed = O.cell_seed(seed_base, ((M, N, K), V, s, "L8-R8"))
-        cases.append((s, O.build_sddmm_case(M, N, K, V, s, BITS, BITS, seed)))
+        seed = O.cell_seed(0, ((mg, N, K), V, s, "L8-R8"))
+        c = O.build_sddmm_case(mg, N, K, V, s, BITS, BITS, seed)
+        lo, hi = rank * (M // V), (rank + 1) * (M // V)
+        offs = c["offsets"]
+        p0, p1 = int(offs[lo]), int(offs[hi])
+        cases.append((s, {"offsets": (offs[lo:hi + 1] - p0).astype(np.int64),
+                          "col_indices": c["col_indices"][p0:p1].copy(),
+                          "a": c["a"][lo * V:hi * V].copy(), "b": c["b"], "seed": seed}))
     return cases
 
 
@@ -72,6 +106,18 @@ def sddmm_bytes(nblk: int) -> int:
     """Algorithmic (compulsory) HBM bytes of one SDDMM launch."""
     return M * K * BITS // 8 + K * N * BITS // 8 + 4 * nblk + 8 * (M // V + 1) + 4 * V * nblk
 
+
+def spmm_bytes(stored, nnz, m, k, n, v, lb, rb):
+    """SURVEY.md §8d SpMM compulsory bytes: LHS values + indices + row bounds + B + C."""
+    return stored * v * lb // 8 + 4 * stored + 16 * (m // v) + k * n * rb // 8 + 4 * m * n
+
+
+CHUNK_PRODUCTS = {(16, 16): 4, (16, 8): 2}  # int8 MMA products per logical product on B200
+
+
+# ---------------------------------------------------------------------------------------
+# measurement helpers
+# ---------------------------------------------------------------------------------------
 
 class ClockSampler:
     """NVML sampling of SM clocks + throttle reasons while the GPU works."""
@@ -132,116 +178,130 @@ def load_traffic(kernel_key: str):
     return None
 
 
-def _structs(tensors, nblk, Nn):
-    """C-ABI structs over device tensors (a words, b^T words, offsets, cols, out)."""
-    a_d, b_d, o_d, c_d, out = tensors
-    a = Nn.McDense(M, K, BITS, Nn.MC_ROW_MAJOR, Nn.ptr(a_d))
-    b = Nn.McDense(K, N, BITS, Nn.MC_COL_MAJOR, Nn.ptr(b_d))
-    pat = Nn.McBcrs(M, N, V, 0, nblk, Nn.ptr(o_d), Nn.ptr(c_d))
-    st = (a, b, pat, out)
-    _KEEP.append(tensors)
-    return st
+class Ctx:
+    """Per-rank device context: torch, the library, the stream, the process group."""
 
+    def __init__(self):
+        import torch
+        from paper_2209_06979_b200 import _native as Nn
+        self.torch, self.Nn = torch, Nn
+        self.rank, self.world, self.local = dist_info()
+        if self.world > 1:
+            ndev = torch.cuda.device_count()
+            if self.world > ndev or self.local >= ndev:
+                raise SystemExit(f"bench.py: refusing {self.world} ranks on {ndev} visible GPU(s) -- "
+                                 "every rank needs its own device")
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=self.dev)
+            self.dist = dist
+        self.lib = Nn.lib()
+        self.stream = torch.cuda.current_stream()
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=self.dev)
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.dist is None:
+            return x
+        t = self.torch.tensor([x], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_true(self, ok: bool) -> bool:
+        if self.dist is None:
+            return ok
+        t = self.torch.tensor([1 if ok else 0], device=self.dev, dtype=self.torch.int32)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    def capture(self, fn):
+        """CUDA graph of fn(stream) (fn issues libmcube launches on the given stream)."""
+        torch = self.torch
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(self.stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(g, stream=cap):
+                fn(cap)
+        self.stream.wait_stream(cap)
+        torch.cuda.synchronize()
+        return g
+
+    def time_flushed(self, g, reps: int) -> float:
+        """Median device time (ms) of graph g, L2 flushed before every replay (events bracket
+        the replay only), 2 untimed replays first; max over ranks."""
+        torch, Nn = self.torch, self.Nn
+        e0 = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
+        e1 = [torch.cuda.Event(enable_timing=True) for _ in range(reps)]
+        sp = Nn.stream_ptr(self.stream)
+        self.barrier()
+        for i in range(reps + 2):
+            self.lib.mc_l2_flush(Nn.ptr(self.flush), self.flush.numel(), sp)
+            if i >= 2:
+                e0[i - 2].record(self.stream)
+            g.replay()
+            if i >= 2:
+                e1[i - 2].record(self.stream)
+        torch.cuda.synchronize()
+        ms = float(np.median([a.elapsed_time(b) for a, b in zip(e0, e1)]))
+        return self.max_over_ranks(ms)
+
+
+def measure_int8_peak(ctx) -> dict:
+    """Dense int8 tensor-core peak on this box: cuBLASLt int8 GEMM (torch._int_mm) at 8192^3,
+    best of 10 (the int8 analogue of MEASURED_PEAKS.json's cuBLAS bf16 figure)."""
+    torch = ctx.torch
+    try:
+        n = 8192
+        a = torch.randint(-127, 128, (n, n), dtype=torch.int8, device=ctx.dev)
+        b = torch.randint(-127, 128, (n, n), dtype=torch.int8, device=ctx.dev).t().contiguous().t()
+        for _ in range(3):
+            torch._int_mm(a, b)
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b
+        return {"int8_tops": 2 * n ** 3 / (best * 1e-3) / 1e12, "how": "torch._int_mm (cuBLASLt) 8192^3, best of 10",
+                "kind": "measured"}
+    except Exception as e:  # pragma: no cover - depends on the box
+        _, bf16, _ = measured_peaks()
+        return {"int8_tops": 2 * bf16, "how": f"2 x bf16 (int8 GEMM unavailable: {type(e).__name__})",
+                "kind": "assumed"}
+
+
+# ---------------------------------------------------------------------------------------
+# C2: the headline SDDMM sweep
+# ---------------------------------------------------------------------------------------
 
 _KEEP = []  # device tensors behind the C structs (kept alive for the whole run)
 
 
-def _clone_problem(base, torch):
-    """Another device-resident copy of one problem (same bytes, distinct addresses)."""
-    for tensors in _KEEP:
-        if tensors[4] is base[3]:
-            break
-    else:
-        raise RuntimeError("unknown problem")
-    from paper_2209_06979_b200 import _native as Nn
-    new = [t.clone() for t in tensors[:4]] + [torch.empty_like(tensors[4])]
-    return _structs(new, base[2].n_blocks, Nn)
+def _sddmm_structs(tensors, nblk, Nn):
+    a_d, b_d, o_d, c_d, out = tensors
+    a = Nn.McDense(M, K, BITS, Nn.MC_ROW_MAJOR, Nn.ptr(a_d))
+    b = Nn.McDense(K, N, BITS, Nn.MC_COL_MAJOR, Nn.ptr(b_d))
+    pat = Nn.McBcrs(M, N, V, 0, nblk, Nn.ptr(o_d), Nn.ptr(c_d))
+    _KEEP.append(tensors)
+    return (a, b, pat, out), tensors
 
 
-REF_ROW_FRACTION = 0.25  # reference-arm step = the first quarter of every C2 problem's rows
-
-
-def cpu_sweep(cases, fraction=1.0):
-    """The reference algorithm on the host (oracle port): one C2 sweep over the first
-    `fraction` of each problem's vector rows (rows carry equal work in the synthetic
-    patterns, so the rate is that of the full sweep); returns the ops computed."""
-    import oracle as O
-    ops = 0
-    for s, c in cases:
-        vr = max(1, int(round((M // V) * fraction)))
-        offs = c["offsets"][:vr + 1]
-        cols = c["col_indices"][:int(offs[-1])]
-        O.sddmm(c["a"][:vr * V], c["b"], offs, cols, V, BITS, BITS)
-        ops += 2 * V * K * int(offs[-1])
-    return ops
-
-
-def blas_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        info = threadpool_info()
-        return max([i.get("num_threads", 1) for i in info] or [1])
-    except Exception:
-        return os.cpu_count() or 1
-
-
-def run_reference(args):
-    rank, world, _ = dist_info()
-    if rank != 0:
-        return
-    cases = build_c2(0)
-    for _ in range(args.warmup):
-        cpu_sweep(cases, REF_ROW_FRACTION)
-    times, ops = [], 0
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        ops = cpu_sweep(cases, REF_ROW_FRACTION)
-        times.append(time.perf_counter() - t0)
-    total = sum(times)
-    value = ops * args.steps / total / 1e12
-    cores = blas_threads()
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "TOPS",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-        "config": {"workload": "C2 SDDMM L8-R8 V=8 M=N=4096 K=256 sparsity 50/70/90/95/98%",
-                   "global_batch": 1, "parallelism": "host"},
-        "cpu_baseline": {"value": value, "unit": "TOPS", "cores": cores, "kind": "port",
-                         "sample": f"first {REF_ROW_FRACTION:.0%} of the vector rows of each C2 problem per "
-                                   "step (oracle/magicube_ref.sddmm, float64 BLAS gathers, reference int32 "
-                                   "semantics); TOPS counts the sampled blocks"},
-        "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def run_ours(args):
-    import torch
-
+def bench_c2(ctx, args, status):
     import paper_2209_06979_b200 as mc
     from paper_2209_06979_b200 import _device as D
-    from paper_2209_06979_b200 import _native as Nn
-
-    rank, world, local = dist_info()
-    # one process per GPU; MCUBE_BENCH_BACKEND=gloo lets several ranks share one device
-    # (used to exercise the N > 1 code path on a single-GPU box)
-    backend = os.environ.get("MCUBE_BENCH_BACKEND", "nccl")
-    if backend != "nccl":
-        local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
-    lib = Nn.lib()
-    stream = torch.cuda.current_stream()
-    sp = Nn.stream_ptr(stream)
-
-    cases = build_c2(rank)  # weak scaling: every rank owns one independent C2 sweep
+    torch, Nn, lib = ctx.torch, ctx.Nn, ctx.lib
+    dev, stream = ctx.dev, ctx.stream
+    cases = c2_rank_cases(ctx.rank, ctx.world)
     probs = []
     for s, c in cases:
         pat = mc.BcrsMatrix(M, N, V, c["offsets"], c["col_indices"],
@@ -256,66 +316,66 @@ def run_ours(args):
                    torch.from_numpy(np.asarray(c["col_indices"], dtype=np.uint32).view(np.int32)).to(dev),
                    torch.empty(nblk * V, dtype=torch.int32, device=dev)]
         foot = sum(t.numel() * t.element_size() for t in tensors)
-        probs.append(dict(s=s, p=p, dev=_structs(tensors, nblk, Nn), nblk=nblk, ops=2 * V * K * nblk,
+        st, tens = _sddmm_structs(tensors, nblk, Nn)
+        probs.append(dict(s=s, p=p, copies=[st], tensors=[tens], nblk=nblk, ops=2 * V * K * nblk,
                           bytes=sddmm_bytes(nblk), foot=foot, c=c))
-        probs[-1]["out"] = probs[-1]["dev"][3]
-    status = D.status_word()
-
-    def launch(pr, copy=0):
-        a, b, pat, out = pr["copies"][copy]
-        Nn.check(lib.mc_sddmm(a, b, pat, Nn.ptr(out), Nn.ptr(status), sp))
-
-    # Cold-L2 discipline: every problem gets enough device-resident copies of its inputs
-    # and output that one rotation touches more than COLD_BYTES (> 2x the 126 MB L2), so a
-    # launch never finds its operands in L2 from an earlier launch -- no flush kernel
-    # between timed launches (SURVEY.md §8d timing rules: "inputs larger than L2").
+    # cold-L2 discipline: enough device copies per problem that one rotation touches more
+    # than COLD_BYTES (> 2x the 126 MB L2): no launch finds its operands in L2 from an
+    # earlier launch, and no flush kernel sits between timed launches
     for pr in probs:
-        foot = pr["foot"]
-        ncopy = max(2, -(-COLD_BYTES // foot))
-        base = pr["dev"]
-        pr["copies"] = [base] + [_clone_problem(base, torch) for _ in range(ncopy - 1)]
+        ncopy = max(2, -(-COLD_BYTES // pr["foot"]))
+        base = pr["tensors"][0]
+        for _ in range(ncopy - 1):
+            new = [t.clone() for t in base[:4]] + [torch.empty_like(base[4])]
+            st, tens = _sddmm_structs(new, pr["nblk"], Nn)
+            pr["copies"].append(st)
+            pr["tensors"].append(tens)
         pr["ncopy"] = ncopy
     step_copies = max(2, -(-COLD_BYTES // sum(pr["foot"] for pr in probs)))
 
-    # correctness gate before timing: bit-exact vs the oracle on sampled rows (every copy
-    # of the largest problem and copy 0 of the others)
+    def launch(pr, cidx, sp):
+        a, b, pat, out = pr["copies"][cidx]
+        Nn.check(lib.mc_sddmm(a, b, pat, Nn.ptr(out), Nn.ptr(status), sp))
+
+    # correctness gate before timing: every copy of every problem launched once, then
+    # bit-exact vs the oracle on sampled rows (every copy of the largest problem)
+    sp0 = Nn.stream_ptr(stream)
     for pr in probs:
         for cidx in range(pr["ncopy"]):
-            launch(pr, cidx)
+            launch(pr, cidx, sp0)
     D.fetch_status(status)
+    fault = None
+    if args.inject_fault:  # negative control: flip one output bit of copy 0 of the 50 % problem
+        out0 = probs[0]["copies"][0][3]
+        fault = int(out0.numel() // 2)
+        out0[fault] ^= 1
     import oracle as O
+    exact = True
     for pr in probs:
         c = pr["c"]
         offs = c["offsets"]
         outs = [pr["copies"][0][3]] + ([cp[3] for cp in pr["copies"][1:]] if pr is probs[0] else [])
-        for r in range(0, M // V, 61):
+        for r in list(range(0, M // V, 61)) + ([int(np.searchsorted(offs, fault // V, side="right")) - 1]
+                                               if fault is not None and pr is probs[0] else []):
             lo, hi = int(offs[r]), int(offs[r + 1])
             want = O.sddmm(c["a"][r * V:(r + 1) * V], c["b"], np.array([0, hi - lo]),
                            c["col_indices"][lo:hi], V, BITS, BITS)
             for out in outs:
-                got = out[lo * V:hi * V].cpu().numpy()
-                assert (got == want).all(), f"SDDMM mismatch at sparsity {pr['s']} row {r}"
+                exact &= bool((out[lo * V:hi * V].cpu().numpy() == want).all())
+    exact = ctx.all_true(exact)
+    if fault is None and not exact:
+        raise SystemExit("bench.py: C2 SDDMM output differs from the oracle")
 
-    peak_hbm, _, peak_kind = measured_peaks()
     n_launch = len(probs)
 
     def capture(seq):
-        """One CUDA graph replaying the launches in `seq` [(problem, copy)] back to back."""
-        g = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(stream)
-        with torch.cuda.stream(cap):
+        def body(cap):
             csp = Nn.stream_ptr(cap)
-            with torch.cuda.graph(g, stream=cap):
-                for pr, cidx in seq:
-                    a, b, pat, out = pr["copies"][cidx]
-                    Nn.check(lib.mc_sddmm(a, b, pat, Nn.ptr(out), Nn.ptr(status), csp))
-        stream.wait_stream(cap)
-        torch.cuda.synchronize()
-        return g
+            for pr, cidx in seq:
+                launch(pr, cidx, csp)
+        return ctx.capture(body)
 
     def timed(g, reps=1):
-        """Device time (ms) of `reps` back-to-back replays of graph g (events at the ends)."""
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -325,96 +385,36 @@ def run_ours(args):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1)
 
-    # headline: K steps, one step = the 5-sparsity sweep, rotating input copies per step
     lib.mc_launch_count(1)
     warm = capture([(pr, w % pr["ncopy"]) for w in range(args.warmup) for pr in probs])
     main = capture([(pr, (step % step_copies) % pr["ncopy"]) for step in range(args.steps) for pr in probs])
     launches = int(lib.mc_launch_count(0)) - n_launch * args.warmup  # libmcube kernels in the timed graph
-    # per-launch device times (same cold discipline), for the sweep table and the roofline
-    per_reps = 3
     singles = [capture([(pr, cidx) for cidx in range(pr["ncopy"])]) for pr in probs]
 
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
     timed(warm)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    with ClockSampler(local) as clk:
+    ctx.barrier()
+    with ClockSampler(ctx.local) as clk:
         total_ms_local = timed(main)
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
+    per_reps = 3
     per_launch = []
     for g, pr in zip(singles, probs):
-        timed(g)  # warm the graph
-        per_launch.append(timed(g, per_reps) / (per_reps * pr["ncopy"]))
+        timed(g)
+        per_launch.append(ctx.max_over_ranks(timed(g, per_reps) / (per_reps * pr["ncopy"])))
     D.fetch_status(status)
-    total_ms = total_ms_local
-    if world > 1:
-        t = torch.tensor([total_ms_local], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = ctx.max_over_ranks(total_ms_local)
     ops_step = sum(pr["ops"] for pr in probs)
-    value = ops_step * world * args.steps / (total_ms * 1e-3) / 1e12
-
-    # roofline of the dominant kernel (the 50% launch, largest bytes)
-    dom = int(np.argmax([pr["bytes"] for pr in probs]))
-    dom_ms = per_launch[dom]
-    achieved = probs[dom]["bytes"] / (dom_ms * 1e-3) / 1e9
-    sweep = {f"{pr['s']:.2f}": {
-        "tops": pr["ops"] / (per_launch[j] * 1e-3) / 1e12,
-        "us": 1e3 * per_launch[j],
-        "hbm_gbs": pr["bytes"] / (per_launch[j] * 1e-3) / 1e9,
-        "roofline_frac": (pr["bytes"] / (per_launch[j] * 1e-3) / 1e9) / peak_hbm,
-        "copies": pr["ncopy"],
-        "kernel": ("sddmm_tc_kernel (tcgen05 kind::i8 dense tile)" if pr["nblk"] * V / (M * N) >= 0.08
-                   else "sddmm_kernel (mma.sync gather)"),
-    } for j, pr in enumerate(probs)}
-
-    # end-to-end through the C ABI with pinned host buffers
-    e2e = run_e2e(args, probs, lib, Nn, torch, dev, stream, world)
-
-    # validation-only collective (outside every timed region): NCCL all-gather of each
-    # rank's output checksums + sampled-row verdicts
-    validation = {"ranks": world, "sampled_rows_exact": True}
-    if world > 1:
-        sums = torch.tensor([int(pr["out"].to(torch.int64).sum().item()) for pr in probs] + [1],
-                            dtype=torch.int64, device=dev)
-        gathered = [torch.empty_like(sums) for _ in range(world)]
-        dist.all_gather(gathered, sums)
-        validation["checksums"] = [g[:-1].tolist() for g in gathered]
-        validation["sampled_rows_exact"] = bool(all(int(g[-1]) == 1 for g in gathered))
-
-    line = {
-        "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
-        "config": {"workload": "C2 SDDMM L8-R8 V=8 M=N=4096 K=256 sparsity 50/70/90/95/98%",
-                   "global_batch": world, "launches_per_step": n_launch,
-                   "l2": f"cold: inputs larger than L2 ({step_copies} rotating device copies of the "
-                         f"sweep's operands and outputs, >= {COLD_BYTES >> 20} MiB per rotation)",
-                   "parallelism": f"independent C2 sweep per rank x{world}"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak_hbm, "unit": "GB/s",
-                     "frac": achieved / peak_hbm, "traffic": load_traffic("sddmm_c2_s0.50"),
-                     "kernel": "sddmm_tc_kernel<8, 32> (tcgen05 kind::i8) @ sparsity 0.50",
-                     "algorithmic_bytes": probs[dom]["bytes"], "peak_kind": peak_kind},
-        "sweep": sweep,
-        "e2e": e2e,
-        "validation": validation,
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
-    }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(probs)
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    value = ops_step * ctx.world * args.steps / (total_ms * 1e-3) / 1e12
+    checksums = [int(pr["copies"][0][3].to(torch.int64).sum().item()) for pr in probs]
+    return dict(probs=probs, value=value, total_ms=total_ms, per_launch=per_launch, launches=launches,
+                clocks=clk.summary(), step_copies=step_copies, exact=exact, fault=fault, checksums=checksums)
 
 
-def run_e2e(args, probs, lib, Nn, torch, dev, stream, world):
-    """Same sweep through mc_sddmm with host<->device copies inside the timed region."""
+def run_e2e(ctx, args, probs, fault=None):
+    """The C2 sweep through mc_sddmm with host<->device copies inside the timed region."""
     from paper_2209_06979_b200 import _device as D
+    torch, Nn, lib, dev, stream = ctx.torch, ctx.Nn, ctx.lib, ctx.dev, ctx.stream
     host, devb, structs = [], [], []
     h2d = d2h = 0
     for pr in probs:
@@ -450,6 +450,7 @@ def run_e2e(args, probs, lib, Nn, torch, dev, stream, world):
     for _ in range(max(1, args.warmup)):
         step()
     torch.cuda.synchronize()
+    ctx.barrier()
     s0 = torch.cuda.Event(enable_timing=True)
     s1 = torch.cuda.Event(enable_timing=True)
     s0.record(stream)
@@ -461,35 +462,378 @@ def run_e2e(args, probs, lib, Nn, torch, dev, stream, world):
         stream.wait_stream(st)
     s1.record(stream)
     torch.cuda.synchronize()
-    ms = s0.elapsed_time(s1)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    # results copied back must equal the device-resident run
-    for (hs, (d, out_d), _), pr in zip(zip(host, devb, structs), probs):
-        assert torch.equal(hs[4], pr["out"].cpu())
+    ms = ctx.max_over_ranks(s0.elapsed_time(s1))
+    for (hs, (d, out_d), _), pr in zip(zip(host, devb, structs), probs):  # copies back == device run
+        assert torch.equal(hs[4], pr["tensors"][0][4].cpu()) or (fault is not None and pr is probs[0])
     ops = sum(pr["ops"] for pr in probs)
-    return {"value": ops * world * args.steps / (ms * 1e-3) / 1e12, "unit": "TOPS",
+    return {"value": ops * ctx.world * args.steps / (ms * 1e-3) / 1e12, "unit": "TOPS",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "ms_per_step": ms / args.steps,
             "path": "mc_sddmm (C ABI), pinned host buffers, one stream per sweep cell (copies overlap kernels)"}
 
 
-def cpu_baseline(probs):
-    """Oracle port on the host cores over a bounded sample (~10-30 s of CPU work)."""
-    cases = [(pr["s"], pr["c"]) for pr in probs]
+# ---------------------------------------------------------------------------------------
+# C3 / C5: SpMM cells split into vector-row panels
+# ---------------------------------------------------------------------------------------
+
+def _spmm_panel_device(ctx, c, m, k, lb, rb):
+    """This rank's rebased row panel of an SpMM case as device tensors (+ panel bounds)."""
+    import paper_2209_06979_b200 as mc
+    from paper_2209_06979_b200 import shard
+    torch = ctx.torch
+    host = mc.SrBcrsMatrix(m, k, c["v"], c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                           mc.PackedArray(c["values"].size, lb, True, mc.pack_values(c["values"], lb)),
+                           shuffled=c["shuffled"])
+    parts = shard.row_panels(host, ctx.world)
+    lo, hi = parts[ctx.rank]
+    sub = shard.srbcrs_panel(host, lo, hi) if ctx.world > 1 else host
+    t = lambda x, dt: torch.from_numpy(np.ascontiguousarray(np.asarray(x)).view(dt)).to(ctx.dev)
+    lhs = mc.SrBcrsMatrix(sub.scalar_rows, k, c["v"], c["stride"], t(sub.row_begin, np.int64),
+                          t(sub.row_end, np.int64), t(sub.col_indices, np.int32),
+                          mc.PackedArray(sub.values.count, lb, True, t(sub.values.words, np.int32)),
+                          shuffled=c["shuffled"])
+    rhs = mc.PackedMatrix(k, c["n"], rb, mc.qint.ROW_MAJOR, True, t(mc.pack_values(c["rhs"], rb), np.int32))
+    return mc.SpmmProblem(lhs, rhs), (lo, hi)
+
+
+def _spmm_cell(ctx, c, m, k, n, v, lb, rb, reps, peaks, check_rows):
+    """Time one SpMM problem split into row panels; sampled rows vs the oracle."""
+    import oracle as O
+    import paper_2209_06979_b200 as mc
+    torch = ctx.torch
+    p, (lo, hi) = _spmm_panel_device(ctx, c, m, k, lb, rb)
+    out = torch.empty((p.lhs.scalar_rows, n), dtype=torch.int32, device=ctx.dev)
+    mc.kernels.spmm_device(p, out=out)  # status-checked launch
+    need = ctx.Nn.ctypes.c_size_t(0)
+    ctx.Nn.check(ctx.lib.mc_spmm_workspace(mc._device.srbcrs_struct(p.lhs)[0],
+                                           mc._device.dense_struct(p.rhs)[0], ctx.Nn.ctypes.byref(need)))
+    path = "densify + gemm_tc_kernel (tcgen05)" if need.value else "spmm_kernel (mma.sync gather)"
+    g = ctx.capture(lambda cap: mc.kernels.spmm_device(p, out=out, stream=cap, check_status=False))
+    ms = ctx.time_flushed(g, reps)
+    rows_local = hi - lo
+    rows = sorted(set(range(0, rows_local, max(1, rows_local // check_rows))) | {rows_local - 1}) \
+        if rows_local else []
+    ok = True
+    if rows:
+        want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], v, c["stride"],
+                      c["shuffled"], lb, c["rhs"], rb, k, rows=[lo + r for r in rows])
+        got = torch.cat([out[r * v:(r + 1) * v] for r in rows]).cpu().numpy()
+        ok = bool((got == want).all())
+    ok = ctx.all_true(ok)
+    nnz = int((c["row_end"] - c["row_begin"]).sum())
+    stored = int(c["col_indices"].size)
+    ops = 2 * v * n * nnz
+    byts = spmm_bytes(stored, nnz, m, k, n, v, lb, rb)
+    hbm, int8 = peaks
+    t_tc = ops * CHUNK_PRODUCTS.get((lb, rb), 1) / (int8 * 1e12)
+    t_hbm = byts / (hbm * 1e9)
+    del out, g
+    return {"us": ms * 1e3, "tops": ops / (ms * 1e-3) / 1e12, "roofline_frac": max(t_tc, t_hbm) / (ms * 1e-3),
+            "bound": "hbm" if t_hbm >= t_tc else "tensor", "bytes": byts, "ops": ops, "path": path,
+            "exact_sampled_rows": ok}
+
+
+def bench_c3(ctx, peaks, reps):
+    import oracle as O
+    cells = {}
+    tot_ops = tot_ms = 0.0
+    m = k = 4096
+    n = 512
+    for lb, rb in C3_PAIRS:
+        for v in (2, 4, 8):
+            for s in C3_SPARSITIES:
+                seed = O.cell_seed(0, ((m, n, k), v, s, f"L{lb}-R{rb}"))
+                c = O.build_spmm_case(m, n, k, v, s, lb, rb, seed)
+                r = _spmm_cell(ctx, c, m, k, n, v, lb, rb, reps, peaks, check_rows=8)
+                cells[f"L{lb}-R{rb} V={v} s={s:.2f}"] = r
+                tot_ops += r["ops"]
+                tot_ms += r["us"] * 1e-3
+    fr = [r["roofline_frac"] for r in cells.values()]
+    return {"workload": "C3 SpMM M=K=4096 N=512, 5 pairs x V{2,4,8} x sparsity{70,90,98}%"
+                        + (f", each cell split into {ctx.world} row panels" if ctx.world > 1 else ""),
+            "tops_sweep": tot_ops / (tot_ms * 1e-3) / 1e12, "us_sweep": tot_ms * 1e3,
+            "roofline_frac_median": float(np.median(fr)), "roofline_frac_min": float(min(fr)),
+            "roofline_frac_max": float(max(fr)),
+            "exact_sampled_rows": all(r["exact_sampled_rows"] for r in cells.values()),
+            "l2": "flushed (256 MiB write + read) before every launch", "cells": {
+                key: {x: r[x] for x in ("us", "tops", "roofline_frac", "bound", "path")} for key, r in cells.items()}}
+
+
+def bench_c5(ctx, peaks, reps):
+    import oracle as O
+    cfg = C5
+    m, k, n, v, s, lb, rb = (cfg[x] for x in ("m", "k", "n", "v", "sparsity", "lb", "rb"))
+    seed = O.cell_seed(0, ((m, n, k), v, s, f"L{lb}-R{rb}"))
+    t0 = time.time()
+    c = O.build_spmm_case(m, n, k, v, s, lb, rb, seed)
+    build_s = time.time() - t0
+    r = _spmm_cell(ctx, c, m, k, n, v, lb, rb, reps, peaks, check_rows=16)
+    r.update(workload=f"C5 SpMM L8-R4 V=8 S=32 shuffled M=K=32768 N=2048 95%"
+                      + (f", split into {ctx.world} row panels" if ctx.world > 1 else ""),
+             build_s=build_s, kernel="spmm_kernel<8, 4, 8, 4> (mma.sync gather)")
+    return r
+
+
+# ---------------------------------------------------------------------------------------
+# C4: fused sparse attention, batch x head split
+# ---------------------------------------------------------------------------------------
+
+def bench_c4(ctx, peaks, reps):
+    import oracle as O
+    import paper_2209_06979_b200 as mc
+    from paper_2209_06979_b200 import shard
+    torch = ctx.torch
+    B, H, L, d, s = (C4[x] for x in ("batch", "heads", "seq", "d", "sparsity"))
+    seed = O.cell_seed(0, ((L, d, H), 8, s, "L8-R8"))
+    offs, cols, _ = O.synthetic_bcrs(L, L, 8, s, seed, 8)
+    mask = mc.BcrsMatrix(L, L, 8, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * 8), 8))
+    cfg = mc.AttentionConfig(L, 8, 8, mask, head_dim=d, num_heads=H)
+    lo, hi = shard.head_ranges(B * H, ctx.world)[ctx.rank]
+    nh = hi - lo
+    g = torch.Generator(device=ctx.dev).manual_seed(seed + lo)
+    q, k, vv = (torch.randn((nh, L, d), device=ctx.dev, generator=g).half() for _ in range(3))
+    run = mc.AttentionRunner(cfg, nh, mode="fast")
+    run(q, k, vv, check=True)
+    ctx.lib.mc_launch_count(1)
+    graph = ctx.capture(lambda cap: run(q, k, vv, stream=cap))
+    launches = int(ctx.lib.mc_launch_count(0))
+    ms = ctx.time_flushed(graph, reps)
+    ok = True
+    for h in (0, nh - 1):
+        ref = O.attention(q[h].double().cpu().numpy(), k[h].double().cpu().numpy(), vv[h].double().cpu().numpy(),
+                          offs, cols, L, d, 8, 8)
+        ok &= float(np.abs(run.out[h].double().cpu().numpy() - ref["output"]).max()) <= mc.attention.FAST_MODE_TOLERANCE
+    ok = ctx.all_true(ok)
+    nblk = int(offs[-1])
+    ops = B * H * 4 * 8 * d * nblk
+    byts = B * H * (3 * L * d * 2 + L * d * 2) + 8 * (L // 8 + 1) + 4 * nblk
+    hbm, int8 = peaks
+    t_roof = max(byts / (hbm * 1e9), ops / (int8 * 1e12))
+    return {"workload": f"C4 fused 8b-8b sparse attention B={B} H={H} L={L} d={d} 90% (fp16 in/out, fast mode)"
+                        + (f", {B * H} (batch, head) pairs split over {ctx.world} ranks" if ctx.world > 1 else ""),
+            "seq_per_s": B / (ms * 1e-3), "ms_per_layer": ms, "tops": ops / (ms * 1e-3) / 1e12,
+            "roofline_frac": t_roof / (ms * 1e-3), "bound": "hbm", "bytes": byts,
+            "launches_per_layer": launches, "sampled_heads_within_tolerance": ok,
+            "tolerance": mc.attention.FAST_MODE_TOLERANCE, "l2": "flushed before every layer",
+            "kernels": "absquant_f16_kernel (cluster quantisation) + score_softmax_kernel<FAST, MIX>"}
+
+
+# ---------------------------------------------------------------------------------------
+# the reference's CPU path (qsparse from baseline/_ref), or the oracle port
+# ---------------------------------------------------------------------------------------
+
+def _reference_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "qsparse"))
+
+
+_W = {}
+
+
+def _ref_worker_init(kind):
+    if _W.get("kind") == kind:  # forked from an initialised parent
+        return
+    for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[var] = "1"
+    if kind == "reference":
+        sys.path.insert(0, os.path.join(REF_DIR))
+        from qsparse import bench as rb
+        from qsparse import kernels as kn
+        from qsparse import sparse_format as sf
+        probs = []
+        for s in SPARSITIES:
+            spec = rb.SweepSpec("sddmm", [(M, N, K)])
+            seed = rb._cell_seed(spec, ((M, N, K), V, s, "L8-R8"))
+            prob, _, _, _ = rb._build_sddmm(spec, (M, N, K), V, s, BITS, BITS, seed)
+            probs.append(prob)
+        _W.update(kind=kind, kn=kn, sf=sf, probs=probs, a_dense=[p.a.to_dense() for p in probs])
+    else:
+        _W.update(kind=kind, cases=c2_rank_cases(0, 1))
+
+
+def _ref_rows(job):
+    """Vector rows [lo, hi) of C2 problem i through the reference (or the port); returns ops."""
+    i, lo, hi = job
+    if _W["kind"] == "reference":
+        kn, sf = _W["kn"], _W["sf"]
+        p = _W["probs"][i]
+        pat = p.out_pattern
+        offs = np.asarray(pat.row_offsets)
+        p0, p1 = int(offs[lo]), int(offs[hi])
+        vals = sf.PackedArray.from_values(np.ones((p1 - p0) * V, dtype=np.int64), 8)
+        sub_pat = sf.BcrsMatrix((hi - lo) * V, N, V, offs[lo:hi + 1] - p0, pat.col_indices[p0:p1], vals)
+        a_rows = _W["a_dense"][i][lo * V:hi * V]
+        from qsparse import qint
+        sub = kn.SddmmProblem(qint.pack_dense(a_rows, BITS, qint.ROW_MAJOR), p.b, sub_pat)
+        kn.sddmm(sub)
+        return 2 * V * K * (p1 - p0)
+    import oracle as O
+    s, c = _W["cases"][i]
+    offs = c["offsets"]
+    p0, p1 = int(offs[lo]), int(offs[hi])
+    O.sddmm(c["a"][lo * V:hi * V], c["b"], offs[lo:hi + 1] - p0, c["col_indices"][p0:p1], V, BITS, BITS)
+    return 2 * V * K * (p1 - p0)
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_figures(steps: int, warmup: int, budget_s: float = 20.0):
+    """C2 through the reference's CPU path on the host cores.
+
+    One job = a few vector rows of one C2 problem. A step hands every process one job per
+    sparsity (rows spread over the whole problem), so the step is a bounded row sample of the
+    C2 sweep; TOPS counts the sampled blocks (synthetic rows carry equal work). Also times
+    one process alone (1 core).
+    """
+    import multiprocessing as mpx
+    kind = "reference" if _reference_available() else "port"
+    cores = max(1, os.cpu_count() or 1)
+    rows_per_job = 1 if kind == "reference" else 8
+    ctxm = mpx.get_context("fork")
+    # 1 core first
+    _ref_worker_init(kind)
+    jobs1 = [(i, 0, rows_per_job) for i in range(len(SPARSITIES))]
     t0 = time.perf_counter()
-    reps = 0
-    ops = 0
-    while time.perf_counter() - t0 < 10.0 and reps < 20:
-        ops += cpu_sweep(cases)
-        reps += 1
-    dt = time.perf_counter() - t0
-    return {"value": ops / dt / 1e12, "unit": "TOPS", "cores": blas_threads(), "kind": "port",
-            "sample": f"{reps} full C2 sweeps (oracle/magicube_ref.sddmm, float64 BLAS gathers) "
-                      f"in {dt:.1f} s"}
+    ops1 = sum(_ref_rows(j) for j in jobs1)
+    one_core = ops1 / (time.perf_counter() - t0) / 1e12
+    vrows = M // V
+    with ctxm.Pool(cores, initializer=_ref_worker_init, initargs=(kind,)) as pool:
+        def step(si):
+            jobs = []
+            for w in range(cores):
+                for i in range(len(SPARSITIES)):
+                    lo = ((si * cores + w) * 37 * rows_per_job) % (vrows - rows_per_job)
+                    jobs.append((i, lo, lo + rows_per_job))
+            return sum(pool.map(_ref_rows, jobs, chunksize=len(SPARSITIES)))
+        for w in range(warmup):
+            step(-1 - w)
+        times, ops = [], 0
+        t_start = time.perf_counter()
+        for si in range(steps):
+            t0 = time.perf_counter()
+            ops = step(si)
+            times.append(time.perf_counter() - t0)
+            if time.perf_counter() - t_start > budget_s * 4 and si >= 2:
+                break
+    total = sum(times)
+    value = ops * len(times) / total / 1e12
+    what = ("qsparse.kernels.sddmm (the reference, baseline/_ref)" if kind == "reference"
+            else "oracle/magicube_ref.sddmm (port: baseline/_ref absent)")
+    return {"value": value, "unit": "TOPS", "cores": cores, "kind": kind,
+            "one_core_tops": one_core, "cpu_model": _cpu_model(), "nproc": os.cpu_count(),
+            "steps_timed": len(times), "ms_per_step": 1e3 * total / len(times),
+            "sample": f"per step: {rows_per_job} vector row(s) of each of the 5 C2 problems per process, "
+                      f"{cores} processes (one per host core), rows spread over the problem; {what}; "
+                      "TOPS counts the sampled blocks; one_core_tops = the same rows in one process"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return
+    f = reference_figures(args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": f["value"], "unit": "TOPS",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": f["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": C2_WORKLOAD, "global_batch": 1, "parallelism": f"host, {f['cores']} processes"},
+        "cpu_baseline": {k: f[k] for k in ("value", "unit", "cores", "kind", "sample", "one_core_tops",
+                                           "cpu_model", "nproc")},
+        "e2e": {"value": f["value"], "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+
+def run_ours(args):
+    from paper_2209_06979_b200 import _device as D
+    ctx = Ctx()
+    torch = ctx.torch
+    status = D.status_word()
+    hbm, bf16, peak_kind = measured_peaks()
+    int8 = measure_int8_peak(ctx)
+    peaks = (hbm, int8["int8_tops"])
+    only = set(args.only.split(",")) if args.only else {"c2", "c3", "c4", "c5"}
+
+    c2 = bench_c2(ctx, args, status)
+    probs = c2["probs"]
+    dom = int(np.argmax([pr["bytes"] for pr in probs]))
+    dom_ms = c2["per_launch"][dom]
+    achieved = probs[dom]["bytes"] / (dom_ms * 1e-3) / 1e9
+    sweep = {f"{pr['s']:.2f}": {
+        "tops": pr["ops"] / (c2["per_launch"][j] * 1e-3) / 1e12,
+        "us": 1e3 * c2["per_launch"][j],
+        "hbm_gbs": pr["bytes"] / (c2["per_launch"][j] * 1e-3) / 1e9,
+        "roofline_frac": (pr["bytes"] / (c2["per_launch"][j] * 1e-3) / 1e9) / hbm,
+        "copies": pr["ncopy"],
+        "kernel": ("sddmm_tc_kernel (tcgen05 kind::i8 dense tile)" if pr["nblk"] * V / (M * N) >= 0.08
+                   else "sddmm_kernel (mma.sync gather)"),
+    } for j, pr in enumerate(probs)}
+    e2e = run_e2e(ctx, args, probs, c2["fault"])
+
+    validation = {"ranks": ctx.world, "sampled_rows_exact": c2["exact"]}
+    if c2["fault"] is not None:
+        validation.update(fault_injected=True, fault_detected=not c2["exact"])
+    if ctx.world > 1:  # validation-only collective: every rank's output checksums
+        sums = torch.tensor(c2["checksums"], dtype=torch.int64, device=ctx.dev)
+        gathered = [torch.empty_like(sums) for _ in range(ctx.world)]
+        ctx.dist.all_gather(gathered, sums)
+        validation["checksums"] = [g.tolist() for g in gathered]
+
+    reps = max(5, min(args.steps, 20))
+    extra = {}
+    if "c3" in only:
+        extra["c3"] = bench_c3(ctx, peaks, reps)
+    if "c5" in only:
+        extra["c5"] = bench_c5(ctx, peaks, reps)
+    if "c4" in only:
+        extra["c4"] = bench_c4(ctx, peaks, reps)
+
+    line = {
+        "metric": METRIC, "value": c2["value"], "unit": "TOPS", "n_gpus": ctx.world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": c2["total_ms"] / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "config": {"workload": C2_WORKLOAD + (f", one problem per sparsity of M={M * ctx.world} rows split "
+                                              f"into {ctx.world} vector-row panels" if ctx.world > 1 else ""),
+                   "global_batch": ctx.world, "launches_per_step": len(probs),
+                   "l2": f"cold: inputs larger than L2 ({c2['step_copies']} rotating device copies of the "
+                         f"sweep's operands and outputs, >= {COLD_BYTES >> 20} MiB per rotation)",
+                   "parallelism": f"row panels x{ctx.world}" if ctx.world > 1 else "1 GPU"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": load_traffic("sddmm_c2_s0.50"),
+                     "kernel": "sddmm_tc_kernel<8, 32> (tcgen05 kind::i8) @ sparsity 0.50",
+                     "algorithmic_bytes": probs[dom]["bytes"], "peak_kind": peak_kind},
+        "sweep": sweep,
+        "e2e": e2e,
+        "validation": validation,
+        "gpu_launches": c2["launches"],
+        "clocks": c2["clocks"],
+        "peaks": {"hbm_gbs": hbm, "bf16_tflops": bf16, "int8_tops": int8["int8_tops"], "int8_how": int8["how"],
+                  "int8_kind": int8["kind"]},
+    }
+    line.update(extra)
+    if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
+        f = reference_figures(3, 1, budget_s=10.0)
+        line["cpu_baseline"] = {k: f[k] for k in ("value", "unit", "cores", "kind", "sample", "one_core_tops",
+                                                  "cpu_model", "nproc")}
+    if ctx.rank == 0:
+        print(json.dumps(line), flush=True)
+    if ctx.dist is not None:
+        ctx.dist.destroy_process_group()
+    if c2["fault"] is not None and not validation["fault_detected"]:
+        sys.exit(3)
 
 
 def main():
@@ -499,6 +843,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of c2 (always), c3, c4, c5")
+    ap.add_argument("--inject-fault", action="store_true",
+                    help="flip one device output element before validation (harness negative control)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
