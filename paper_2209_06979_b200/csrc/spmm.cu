@@ -82,9 +82,14 @@ __device__ __forceinline__ int64_t idx_pos(int64_t q, bool shuffled) {
 #ifndef MCUBE_SPMM_MINB
 #define MCUBE_SPMM_MINB 1
 #endif
-template <int LB, int RB, int V, int NS, bool ALIGNED, bool NIB>
+// X16 (RB = 4): a gathered nibble x enters the MMA as the byte 16 x (the nibble moved to the
+// high half of its byte: one mask for odd columns, shift + mask for even ones) instead of
+// a sign-extended s8, so every chunk product is 16 times the true one; the epilogue shifts
+// the int32 accumulators right by 4. Exact while |16 * sum| < 2^31 (spmm_x16_ok).
+template <int LB, int RB, int V, int NS, bool ALIGNED, bool NIB, bool X16 = false>
 __global__ void __launch_bounds__(kWarps * 32, MCUBE_SPMM_MINB)
 spmm_kernel(const SpmmParams p) {
+  static_assert(!X16 || RB == 4, "X16 is the 4-bit RHS operand form");
   using C = SpmmCfg<LB, RB, V, NS, NIB>;
   static_assert(!NIB || (RB == 4 && LB >= 8), "nibble chunks are the 4-bit-width plans of an 8/12/16-bit LHS");
   extern __shared__ __align__(128) uint8_t smem[];
@@ -356,7 +361,14 @@ spmm_kernel(const SpmmParams p) {
       } else {
         uint32_t ev[4], od[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) unpack_s4x8(raw[i][0], ev[i], od[i]);
+        for (int i = 0; i < 4; ++i) {
+          if constexpr (X16) {
+            ev[i] = (raw[i][0] << 4) & 0xF0F0F0F0u;  // 16 x of columns 0, 2, 4, 6
+            od[i] = raw[i][0] & 0xF0F0F0F0u;         // 16 x of columns 1, 3, 5, 7
+          } else {
+            unpack_s4x8(raw[i][0], ev[i], od[i]);
+          }
+        }
         // even columns 0,2,4,6 -> T[0..3]; odd columns 1,3,5,7 -> T[4..7]
         transpose4x4(ev[0], ev[1], ev[2], ev[3], T[0][h][0], T[0][h][1], T[0][h][2], T[0][h][3]);
         transpose4x4(od[0], od[1], od[2], od[3], T[0][h][4], T[0][h][5], T[0][h][6], T[0][h][7]);
@@ -391,6 +403,18 @@ spmm_kernel(const SpmmParams p) {
   cp_async_wait<0>();
 
   // ---- epilogue: exact shift-add recombination + the reference's int32 checks ----
+  if constexpr (X16) {
+#pragma unroll
+    for (int st = 0; st < NS; ++st)
+#pragma unroll
+      for (int c = 0; c < C::LC; ++c)
+#pragma unroll
+        for (int j = 0; j < C::RC; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[st][c][j][q][e] >>= 4;  // exact: every term is a multiple of 16
+  }
   bool overflow = false;
   double alpha = 0.0;
   if (p.out_f16) alpha = p.alpha ? p.alpha[b] : p.alpha_host;
@@ -476,8 +500,17 @@ spmm_kernel(const SpmmParams p) {
   if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
 }
 
+// |16 * sum| < 2^31 for every byte-chunk accumulator: K (>= every row's true vectors),
+// rounded up to the stride, times the largest 16 * |chunk x nibble| term.
+bool spmm_x16_ok(const SpmmParams& p) {
+  const long double sb = static_cast<long double>(((p.K + p.S - 1) / p.S) * p.S);
+  const long double term = p.LB >= 12 ? 255.0L * 8.0L : (p.LB == 4 ? 64.0L : 1024.0L);
+  return sb * term * 16.0L <= 2147483647.0L;
+}
+
 template <int LB, int RB, int V, int NS, bool NIB = false>
 cudaError_t launch_spmm_v(SpmmParams p, cudaStream_t stream) {
+  constexpr bool kX16 = RB == 4 && !NIB;
   using C = SpmmCfg<LB, RB, V, NS, NIB>;
   p.ntiles = (p.N + C::TN - 1) / C::TN;
   p.tasks = static_cast<int64_t>(p.batch) * p.vrows * p.ntiles;
@@ -486,7 +519,11 @@ cudaError_t launch_spmm_v(SpmmParams p, cudaStream_t stream) {
                        ((p.rhs_stride * 4) % 16 == 0);
   const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
   if (grid == 0) return cudaSuccess;
-  if (aligned) {
+  if (aligned && kX16 && spmm_x16_ok(p)) {
+    auto k = spmm_kernel<LB, RB, V, NS, true, NIB, kX16>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (const cudaError_t e = launch_pdl(k, dim3(grid), dim3(kWarps * 32), smem, stream, p)) return e;
+  } else if (aligned) {
     auto k = spmm_kernel<LB, RB, V, NS, true, NIB>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (const cudaError_t e = launch_pdl(k, dim3(grid), dim3(kWarps * 32), smem, stream, p)) return e;
