@@ -142,7 +142,6 @@ spmm_kernel(const SpmmParams p) {
   // copy u of this lane moves 16-byte chunk ch of gathered row kk (CPR chunks per row);
   // computed on demand (a hoisted array per copy costs 5 registers per chunk at CPR = 8)
   auto kk_of = [&](int u) { return (lane + 32 * u) / C::CPR; };
-  auto ch_of = [&](int u) { return (lane + 32 * u) % C::CPR; };
   auto kkp_of = [&](int kk) {  // P^-1 within 8-groups
     return shuffled ? ((kk & ~7) | (((kk & 7) >> 1) | ((kk & 1) << 2))) : kk;
   };
@@ -152,6 +151,12 @@ spmm_kernel(const SpmmParams p) {
   const int64_t a_task_base = (p_begin / p.S) * V * p.S;  // element index of the row's first stride
   const int S = p.S;
   int a_blk = 0, a_within = 0;  // stride-block offset (elements) and offset within stride for pos = 32*step
+
+  // every copy of this lane moves the same 16-byte chunk of its rows (CPR chunks per row)
+  const uint32_t chx = static_cast<uint32_t>((lane % C::CPR) * 16);
+  const uint32_t colofs = static_cast<uint32_t>(c0_bytes) + chx;
+  const bool chunk_ok = c0_bytes + chx < row_bytes;
+  bool bad_idx = false;  // an index >= K that is not the sentinel (flagged once, at the end)
 
   uint32_t nidx[C::CPR];
   auto load_idx = [&](int step) {
@@ -170,16 +175,15 @@ spmm_kernel(const SpmmParams p) {
 #pragma unroll
     for (int u = 0; u < C::CPR; ++u) {
       const int slot = slot_of(kk_of(u));
-      const uint32_t dst = sbase + slot * C::RBYTES + ((ch_of(u) * 16) ^ swz<C::RBYTES>(slot & 3));
-      const uint32_t colofs = static_cast<uint32_t>(c0_bytes) + ch_of(u) * 16;
-      const bool chunk_ok = c0_bytes + ch_of(u) * 16 < row_bytes;
+      const uint32_t dst = sbase + slot * C::RBYTES + (chx ^ swz<C::RBYTES>(slot & 3));
       const uint32_t col = nidx[u];
-      bool ok = col < kdim;
-      if (!ok && col != kSentinel) flag_status(p.status, MC_STATUS_BAD_INDEX);
+      const bool ok = col < kdim;
+      bad_idx |= !ok && col != kSentinel;
       if constexpr (ALIGNED) {
-        const uint32_t nbytes = (ok && chunk_ok) ? 16u : 0u;
-        const uint8_t* src = nbytes ? rhs_b + static_cast<uint64_t>(col) * row_bytes + colofs : rhs_b;
-        cp_async16(dst, src, nbytes);
+        // branch-free: sentinel / out-of-range rows and chunks past N are zero-filled
+        const bool go = ok && chunk_ok;
+        const uint64_t off = go ? static_cast<uint64_t>(col) * row_bytes + colofs : 0ull;
+        cp_async16(dst, rhs_b + off, go ? 16u : 0u);
       } else {
         const int ch = (lane + 32 * u) % C::CPR;
         // generic path: element-wise fetch for rows that are not 16-byte aligned
@@ -498,6 +502,7 @@ spmm_kernel(const SpmmParams p) {
   }
   }  // st
   if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
+  if (bad_idx) flag_status(p.status, MC_STATUS_BAD_INDEX);
 }
 
 // |16 * sum| < 2^31 for every byte-chunk accumulator: K (>= every row's true vectors),
@@ -595,6 +600,7 @@ bool spmm_needs_nibble_chunks(const SpmmParams& p) {
 
 cudaError_t launch_spmm(SpmmParams p, cudaStream_t stream) {
   if (spmm_tc_supported(p)) return launch_spmm_tc(p, stream);
+  if (!spmm_needs_nibble_chunks(p) && spmm_seg_supported(p)) return launch_spmm_seg(p, stream);
   const int key = p.LB * 100 + p.RB;
   switch (key) {
     case 1616: return launch_spmm_lr<16, 16>(p, stream);

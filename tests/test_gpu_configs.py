@@ -140,3 +140,39 @@ def test_attention_head_shards_equal_unsharded():
         r = mc.AttentionRunner(cfg, hi - lo, mode="parity")
         parts.append(r(q[lo:hi].contiguous(), k[lo:hi].contiguous(), vv[lo:hi].contiguous(), check=True).clone())
     assert torch.equal(torch.cat(parts), full)
+
+
+@pytest.mark.parametrize("sparsity", [0.5, 0.95])
+@pytest.mark.parametrize("v", [2, 4, 8])
+@pytest.mark.parametrize("pair,n", [((8, 4), 512), ((8, 4), 96), ((4, 4), 256), ((8, 8), 384), ((8, 8), 48),
+                                    ((16, 8), 256)])
+def test_spmm_segment_path_vs_oracle(pair, n, v, sparsity, monkeypatch):
+    """The TMA gather4 SpMM kernel (spmm_seg.cu, the C5 kernel) forced on small problems:
+    every V, ragged N (zero-filled segment tails), empty / irregular rows."""
+    monkeypatch.setenv("MCUBE_SPMM_PATH", "seg")
+    lb, rb = pair
+    m, k = 256, 640
+    c = O.build_spmm_case(m, n, k, v, sparsity, lb, rb, seed=lb + rb + v + n)
+    lhs = mc.SrBcrsMatrix(m, k, v, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
+                          mc.PackedArray.from_values(c["values"], lb), shuffled=c["shuffled"])
+    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], rb)))
+    want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], v, c["stride"], c["shuffled"], lb,
+                  c["rhs"], rb, k)
+    assert (out == want).all()
+    # irregular rows: empty, full, clustered (the device packer builds the SR-BCRS)
+    rng = np.random.default_rng(v + n)
+    lens = rng.integers(0, k // 3, m // v)
+    lens[::5] = 0
+    lens[1] = k
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(k, size=int(x), replace=False)) for x in lens]).astype(np.uint32)
+    mag = min(c["values"].max(), 127)
+    vals = rng.integers(-mag, mag + 1, cols.size * v)
+    b = mc.BcrsMatrix(m, k, v, offs, cols, mc.PackedArray.from_values(vals, lb))
+    sr = mc.bcrs_to_srbcrs(b, c["stride"])
+    if rb == 4:
+        sr = mc.shuffle_indices(sr)
+    out = mc.spmm(mc.SpmmProblem(sr, mc.pack_dense(c["rhs"], rb)))
+    want = O.spmm(sr.row_begin, sr.row_end, sr.col_indices, sr.values.to_values(), v, sr.stride, sr.shuffled, lb,
+                  c["rhs"], rb, k)
+    assert (out == want).all()
