@@ -504,10 +504,10 @@ def _spmm_cell(ctx, c, m, k, n, v, lb, rb, reps, peaks, check_rows):
     p, (lo, hi) = _spmm_panel_device(ctx, c, m, k, lb, rb)
     out = torch.empty((p.lhs.scalar_rows, n), dtype=torch.int32, device=ctx.dev)
     mc.kernels.spmm_device(p, out=out)  # status-checked launch
-    need = ctx.Nn.ctypes.c_size_t(0)
-    ctx.Nn.check(ctx.lib.mc_spmm_workspace(mc._device.srbcrs_struct(p.lhs)[0],
-                                           mc._device.dense_struct(p.rhs)[0], ctx.Nn.ctypes.byref(need)))
-    path = "densify + gemm_tc_kernel (tcgen05)" if need.value else "spmm_kernel (mma.sync gather)"
+    pid = ctx.Nn.ctypes.c_int32(-1)
+    ctx.Nn.check(ctx.lib.mc_spmm_path(mc._device.srbcrs_struct(p.lhs)[0], mc._device.dense_struct(p.rhs)[0],
+                                      ctx.Nn.ctypes.byref(pid)))
+    path = ctx.Nn.SPMM_PATHS[pid.value]
     g = ctx.capture(lambda cap: mc.kernels.spmm_device(p, out=out, stream=cap, check_status=False))
     ms = ctx.time_flushed(g, reps)
     rows_local = hi - lo
@@ -570,7 +570,7 @@ def bench_c5(ctx, peaks, reps):
     r = _spmm_cell(ctx, c, m, k, n, v, lb, rb, reps, peaks, check_rows=16)
     r.update(workload=f"C5 SpMM L8-R4 V=8 S=32 shuffled M=K=32768 N=2048 95%"
                       + (f", split into {ctx.world} row panels" if ctx.world > 1 else ""),
-             build_s=build_s, kernel="spmm_kernel<8, 4, 8, 4> (mma.sync gather)")
+             build_s=build_s, kernel=r["path"])
     return r
 
 

@@ -113,6 +113,16 @@ int mc_spmm(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n,
  * returns the bytes that path needs (0: the problem always runs on the gather
  * kernels and the workspace may be NULL). Replaces kernels.spmm (kernels.py:293-298). */
 int mc_spmm_workspace(const mc_srbcrs* lhs, const mc_dense* rhs, size_t* bytes);
+/* Which kernel mc_spmm_ws (with the workspace mc_spmm_workspace asked for) runs for this
+ * problem -- for reports and profiling; the result never depends on it. */
+enum {
+  MC_SPMM_PATH_GATHER = 0,  /* spmm.cu: mma.sync, 64-column tasks, cp.async ring        */
+  MC_SPMM_PATH_SEGMENT = 1, /* spmm_seg.cu: mma.sync, 128-byte row-segment tasks        */
+  MC_SPMM_PATH_DENSE = 2,   /* dense.cu + gemm_tc.cu: densify + tcgen05 GEMM            */
+  MC_SPMM_PATH_TC = 3,      /* spmm_tc.cu: tcgen05 gather (MCUBE_SPMM_PATH=tc only)     */
+  MC_SPMM_PATH_NIBBLE = 4   /* spmm.cu with the reference's per-nibble chunk products   */
+};
+int mc_spmm_path(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t* path);
 int mc_spmm_ws(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n,
                int32_t* out, uint32_t* status, void* workspace,
                size_t workspace_bytes, void* stream);

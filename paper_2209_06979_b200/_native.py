@@ -31,6 +31,11 @@ MC_ROW_MAJOR = 0
 MC_COL_MAJOR = 1
 MC_DTYPE_F16, MC_DTYPE_F32, MC_DTYPE_F64 = 0, 1, 2
 MC_ATTN_PARITY, MC_ATTN_FAST = 0, 1
+SPMM_PATHS = {0: "spmm_kernel (mma.sync gather, 64-column tasks)",
+              1: "spmm_seg_kernel (mma.sync, 128-byte row-segment tasks)",
+              2: "densify + gemm_tc_kernel (tcgen05)",
+              3: "spmm_tc_kernel (tcgen05 gather)",
+              4: "spmm_kernel (per-nibble chunk products)"}
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -74,6 +79,7 @@ _SIGNATURES = {
     "mc_spmm": (_i32, [ctypes.POINTER(McSrBcrs), ctypes.POINTER(McDense), _i32, _p, _p, _p]),
     "mc_spmm_workspace": (_i32, [ctypes.POINTER(McSrBcrs), ctypes.POINTER(McDense),
                                  ctypes.POINTER(ctypes.c_size_t)]),
+    "mc_spmm_path": (_i32, [ctypes.POINTER(McSrBcrs), ctypes.POINTER(McDense), ctypes.POINTER(_i32)]),
     "mc_spmm_ws": (_i32, [ctypes.POINTER(McSrBcrs), ctypes.POINTER(McDense), _i32, _p, _p, _p,
                           ctypes.c_size_t, _p]),
     "mc_spmm_batched": (_i32, [ctypes.POINTER(McSrBcrs), _i64, ctypes.POINTER(McDense), _i64, _i32,

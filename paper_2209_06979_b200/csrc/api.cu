@@ -182,6 +182,19 @@ int mc_spmm_workspace(const mc_srbcrs* lhs, const mc_dense* rhs, size_t* bytes) 
   return MC_OK;
 }
 
+int mc_spmm_path(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t* path) {
+  int rc = check_spmm(lhs, rhs, 64);
+  if (rc) return rc;
+  if (!path) return fail(MC_ERR_VALUE, "path must not be NULL");
+  SpmmParams p = spmm_params(lhs, 0, rhs, 0, 1, nullptr, reinterpret_cast<int32_t*>(256), 0, nullptr);
+  if (dense_spmm_workspace(p) > 0) *path = MC_SPMM_PATH_DENSE;
+  else if (spmm_tc_supported(p)) *path = MC_SPMM_PATH_TC;
+  else if (spmm_needs_nibble_chunks(p)) *path = MC_SPMM_PATH_NIBBLE;
+  else if (spmm_seg_supported(p)) *path = MC_SPMM_PATH_SEGMENT;
+  else *path = MC_SPMM_PATH_GATHER;
+  return MC_OK;
+}
+
 int mc_spmm_ws(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n, int32_t* out, uint32_t* status,
                void* workspace, size_t workspace_bytes, void* stream) {
   int rc = check_spmm(lhs, rhs, bs_n);

@@ -298,6 +298,11 @@ cudaError_t launch_lr(const GemmMaps& maps, const SpmmParams& p, cudaStream_t st
 
 // Eligible: one problem (no batch), int32 output only, tile-aligned shapes, density high
 // enough that a dense tensor-core pass beats the L2 gather (crossover measured on C3).
+static bool e_forced_dense() {
+  const char* e = getenv("MCUBE_SPMM_PATH");
+  return e && e[0] == 'd';
+}
+
 bool dense_spmm_eligible(const SpmmParams& p) {
   if (p.batch != 1 || p.out == nullptr || p.out_f16 != nullptr) return false;
   if (p.M % kTM || p.N % 128 || p.K % kKB || p.M <= 0 || p.N <= 0 || p.K <= 0) return false;
@@ -305,6 +310,7 @@ bool dense_spmm_eligible(const SpmmParams& p) {
   // byte-chunk planes only: nibble-chunk plans and strides wider than a staging batch take
   // the gather kernels
   if (spmm_needs_nibble_chunks(p) || !densify_stride_ok(p)) return false;
+  if (!(e_forced_dense()) && spmm_seg_supported(p)) return false;  // the segment gather kernel is faster there
   if ((reinterpret_cast<uintptr_t>(p.rhs_words) & 15) || (reinterpret_cast<uintptr_t>(p.out) & 15)) return false;
   const double density = static_cast<double>(p.stored) * p.V / (static_cast<double>(p.M) * p.K);
   const char* e = getenv("MCUBE_SPMM_PATH");

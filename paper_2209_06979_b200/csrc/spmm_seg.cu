@@ -400,10 +400,19 @@ bool spmm_seg_supported(const SpmmParams& p) {
     if (sb * (p.LB == 4 ? 64.0L : 1024.0L) * 16.0L > 2147483647.0L) return false;
   }
   if (e && e[0] == 's') return true;
-  // big problems only: the C3-sized ones keep the 64-column tasks of spmm.cu (more tasks)
+  // Problems with enough 128-byte row segments to fill the GPU (C5), and the V = 8 cells
+  // at ~90 % sparsity where, measured on C3 (tools/bench_spmm.py c3, forced paths), the
+  // segment kernel beats both the dense-tile GEMM and the 64-column mma.sync tasks for a
+  // 4-bit RHS or a 16-bit LHS (28.6 -> 20.4 us L8-R4 / L4-R4, 40.9 -> 28.6 us L16-R8);
+  // smaller / sparser problems keep spmm.cu's 64-column tasks (more tasks per row).
+  // V < 8: fewer uses per gathered byte than MMA N = 8 provides; the 64-column tasks and
+  // the dense tile win there (C3 V = 2: 64 -> 168 us when forced)
+  if (p.V != 8) return false;
   const int64_t tn = 128 * 8 / p.RB;
   const int64_t tasks = static_cast<int64_t>(p.batch) * p.vrows * ((p.N + tn - 1) / tn);
-  return tasks >= 148LL * 48;
+  if (tasks >= 148LL * 48) return true;
+  const double density = p.stored > 0 ? static_cast<double>(p.stored) * p.V / (static_cast<double>(p.M) * p.K) : 1.0;
+  return (p.RB == 4 || p.LB == 16) && density > 0.05 && density <= 0.11;
 }
 
 cudaError_t launch_spmm_seg(const SpmmParams& p, cudaStream_t stream) {
