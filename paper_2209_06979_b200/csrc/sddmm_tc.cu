@@ -63,6 +63,9 @@ constexpr int kFirstCons = kFirstBuild + kBuildWarps;
 constexpr int kThreads = 32 * (kFirstCons + kConsWarps);
 constexpr int kRowsPerBuilder = 32 / kBuildWarps;       // vector rows per builder warp
 constexpr int kLanesPerRow = 32 / kRowsPerBuilder;      // builder lanes per vector row
+#ifndef MCUBE_BUILDER_LDS128
+#define MCUBE_BUILDER_LDS128 0  // A/B: one LDS.128 of 4 consecutive candidates per lane
+#endif
 constexpr int kRingStride = 516;  // uint32 per row ring (512 + 4 pad)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -291,6 +294,20 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     }
   }
   pdl_wait();
+  // the first tile's A panel and B^T tile go out before the setup barrier: the barriers were
+  // initialised by this thread, and the loads overlap the TMEM allocation, the barrier and
+  // the pattern builders' first window
+  if (warp == 0 && lane == 0 && t0 < t1) {
+    const TileCursor c(t0, p.n_panels, p.n_ctiles);
+    tc::mbar_arrive_expect_tx(a_full, KB * PANEL * KBLK);
+    for (int kb = 0; kb < KB; ++kb)
+      tc::tma_load_2d(sbase + L::OFF_A + kb * PANEL * KBLK, &tmA, a_full, kb * KBLK,
+                      static_cast<int>(c.item * p.M + c.panel * PANEL));
+    tc::mbar_arrive_expect_tx(full_bar(0), KB * kCols * KBLK);
+    for (int kb = 0; kb < KB; ++kb)
+      tc::tma_load_2d(sbase + L::OFF_B + kb * kCols * KBLK, &tmB, full_bar(0), kb * KBLK,
+                      static_cast<int>(c.item * p.N + c.ct * kCols));
+  }
   MC_STAMP(threadIdx.x == 0, 102);
   long long lo = 0, b_lo = 0, b_hi = 0, spec_lo = -1, spec_hi = -1;
   int len = 0, cur = 0, mtop = 0, landed = 0, lo511 = 0, lo63 = 0, depth = 2, c_first = 0;
@@ -304,7 +321,18 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (b_r < p.vrows) {  // the first panel's row offsets: in flight across the setup barrier
       b_lo = p.row_offsets[b_r];
       b_hi = p.row_offsets[b_r + 1];
+      // speculate rows of equal length (exact for the reference generator's patterns): the
+      // first probe window goes out now, overlapping the offsets round trip and the setup
+      // barrier, and is discarded if the offsets disagree
+      spec_lo = (b_r * p.n_blocks) / p.vrows;
+      spec_hi = ((b_r + 1) * p.n_blocks) / p.vrows;
+      const int slen = static_cast<int>(spec_hi - spec_lo);
+      const int2 w = probe_window(slen, b_c00, static_cast<int>(spec_lo & 63));
+      c_first = w.x;
+      if (slen > 0) fetch_chunks(spec_lo, w.x, w.y);
+      mtop = w.y;
     }
+    cp_async_commit();
   }
   MC_STAMP(threadIdx.x == 0, 103);
   MC_STAMP(threadIdx.x == 32 * kFirstBuild, 104);
@@ -324,14 +352,17 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         const int i = static_cast<int>(t - t0);
         const long long item = tc_.item, panel = tc_.panel, ct = tc_.ct, gpanel = tc_.gpanel;
         if (gpanel != cur_panel) {
-          if (n_a > 0) tc::mbar_wait(a_empty, (n_a - 1) & 1);
-          tc::mbar_arrive_expect_tx(a_full, KB * PANEL * KBLK);
-          for (int kb = 0; kb < KB; ++kb)
-            tc::tma_load_2d(sbase + L::OFF_A + kb * PANEL * KBLK, &tmA, a_full, kb * KBLK,
-                            static_cast<int>(item * p.M + panel * PANEL));
+          if (i > 0) {  // tile 0's loads were issued before the setup barrier
+            if (n_a > 0) tc::mbar_wait(a_empty, (n_a - 1) & 1);
+            tc::mbar_arrive_expect_tx(a_full, KB * PANEL * KBLK);
+            for (int kb = 0; kb < KB; ++kb)
+              tc::tma_load_2d(sbase + L::OFF_A + kb * PANEL * KBLK, &tmA, a_full, kb * KBLK,
+                              static_cast<int>(item * p.M + panel * PANEL));
+          }
           ++n_a;
           cur_panel = gpanel;
         }
+        if (i == 0) continue;
         const int s = static_cast<int>(i % kStages);
         const uint32_t u = static_cast<uint32_t>(i / kStages);
         tc::mbar_wait(empty_bar(s), (u & 1) ^ 1);
@@ -394,18 +425,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // leaves the tile (columns strictly increasing), the eight lanes OR their bitmaps with
     // three shuffles, and lane (j, s < 4) writes the QuarterMap of quarter s. No cross-warp
     // synchronisation: each warp arrives on the tile's pfull barrier.
-    if (b_r >= 0 && b_r < p.vrows) {
-      // speculate rows of equal length (exact for the reference generator's patterns):
-      // the window fetch overlaps the offsets round trip and is discarded if wrong
-      spec_lo = (b_r * p.n_blocks) / p.vrows;
-      spec_hi = ((b_r + 1) * p.n_blocks) / p.vrows;
-      const int slen = static_cast<int>(spec_hi - spec_lo);
-      const int2 w = probe_window(slen, b_c00, static_cast<int>(spec_lo & 63));
-      c_first = w.x;
-      if (slen > 0) fetch_chunks(spec_lo, w.x, w.y);
-      mtop = w.y;
-    }
-    cp_async_commit();
+    // (the speculative first window was issued before the setup barrier)
     int64_t cur_panel = -1;
     TileCursor tc_(t0, p.n_panels, p.n_ctiles);
     for (int64_t t = t0; t < t1; ++t, tc_.next()) {
@@ -483,17 +503,15 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       // ---- this tile's bitmap of row j (lanes of the row split the candidates) ----
       const int lim = (len - cur < kCols) ? len - cur : kCols;  // candidates in the tile window
       uint32_t w0 = 0u, w1 = 0u, w2 = 0u, w3 = 0u;
-      bool bad = false, row_live = true;
-      for (int k0 = 0;; k0 += 4 * kLanesPerRow) {
-        const bool act = row_live && k0 < lim;
-        if (!__any_sync(0xffffffffu, act)) break;
-        // candidates [cur + k0, cur + k0 + 16) must have landed
+      bool bad = false;
+      {
+        // the whole candidate window [cur, cur + lim) must have landed: one check per tile
+        // (the prefetch depth keeps two tiles of entries in flight, so this rarely waits)
         const int landed_rel = landed * 64 - lo63;
-        const bool need = act && cur + k0 + 4 * kLanesPerRow > landed_rel && landed_rel < len;
+        const bool need = lim > 0 && cur + lim > landed_rel && landed_rel < len;
         if (__any_sync(0xffffffffu, need)) {
           if (need) {
-            const int last = (cur + k0 + 4 * kLanesPerRow < len) ? cur + k0 + 4 * kLanesPerRow : len;
-            const int c_need = ((lo63 + last - 1) >> 6) + 1;
+            const int c_need = ((lo63 + cur + lim - 1) >> 6) + 1;
             if (c_need > mtop) {
               const int c_cap = ((lo63 + cur) >> 6) + 8;  // never overwrite the cursor's chunk
               const int c_to = (c_need + depth - 1 < c_cap) ? c_need + depth - 1 : c_cap;
@@ -506,11 +524,34 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           __syncwarp();
           landed = mtop_last = mtop;
         }
+      }
+      // 32 candidates of each row per step, 4 consecutive ones per lane (one LDS.128 from a
+      // 16-byte aligned ring position: the up to 3 entries before the cursor have columns
+      // below c0 and are skipped); a step continues while any row of the warp still had a
+      // candidate inside the tile (columns strictly increasing) -- one vote per step
+#if MCUBE_BUILDER_LDS128
+      const int skew = (lo511 + cur) & 3;
+      const int abase = (lo511 + cur) - skew;
+      for (int k0 = 0; k0 < kCols + 4; k0 += 4 * kLanesPerRow) {
+        const int kb = k0 + 4 * sub;  // first candidate of this lane, relative to abase
+        const uint4 q4 = *reinterpret_cast<const uint4*>(rrow + ((abase + kb) & 511));
+        uint32_t c[4] = {q4.x, q4.y, q4.z, q4.w};
+        bool more = true;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = kb + u - skew;  // candidate index relative to the cursor
+          if (k < 0 || k >= lim) c[u] = (k < 0) ? c0 - 1u : kNone;  // before the cursor / past the window
+          const uint32_t off = c[u] - c0;
+          const bool in = off < static_cast<uint32_t>(kCols);
+          more &= (k < 0) || in;
+          bad |= in && c[u] >= static_cast<uint32_t>(p.N);
+#else
+      for (int k0 = 0; k0 < kCols; k0 += 4 * kLanesPerRow) {
         uint32_t c[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int k = k0 + sub + kLanesPerRow * u;
-          c[u] = (act && k < lim) ? rrow[(lo511 + cur + k) & 511] : kNone;
+          c[u] = k < lim ? rrow[(lo511 + cur + k) & 511] : kNone;
         }
         bool more = true;
 #pragma unroll
@@ -519,6 +560,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           const bool in = off < static_cast<uint32_t>(kCols);
           more &= in;
           bad |= in && c[u] >= static_cast<uint32_t>(p.N);
+#endif
           const uint32_t bit = in ? (1u << (off & 31)) : 0u;
           const uint32_t wsel = off >> 5;
           w0 |= wsel == 0 ? bit : 0u;
@@ -526,11 +568,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           w2 |= wsel == 2 ? bit : 0u;
           w3 |= wsel == 3 ? bit : 0u;
         }
-        // a candidate past the tile ends the row: every later candidate is past it too
-        bool done = !more;
-#pragma unroll
-        for (int o = 1; o < kLanesPerRow; o <<= 1) done |= __shfl_xor_sync(0xffffffffu, done, o);
-        row_live &= !done;
+        if (!__any_sync(0xffffffffu, more)) break;
       }
       MC_STAMP(lane == 0 && bw == 0 && i < 5, 65 + 5 * static_cast<int>(i));
       if (bad) flag_status(p.status, MC_STATUS_BAD_INDEX);
