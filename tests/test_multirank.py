@@ -116,3 +116,25 @@ def test_balanced_cuts_and_alignment():
                                   c["values"], shuffled=True)[lo * 2:hi * 2]
             assert (mc.srbcrs_to_dense(sub) == want).all()
     assert shard.head_ranges(512, 8)[3] == (192, 256)
+
+
+def test_bench_c2_row_panels_partition_one_problem():
+    """bench.py at N ranks: every rank's C2 panel is a slice of ONE global problem of
+    M = 4096 * N rows (weak scaling), and the panels tile it exactly."""
+    import bench
+    world = 2
+    panels = [bench.c2_rank_cases(r, world) for r in range(world)]
+    for i, s in enumerate(bench.SPARSITIES):
+        seed = O.cell_seed(0, ((bench.M * world, bench.N, bench.K), bench.V, s, "L8-R8"))
+        g = O.build_sddmm_case(bench.M * world, bench.N, bench.K, bench.V, s, 8, 8, seed)
+        offs = np.concatenate([[0]] + [p[i][1]["offsets"][1:] + sum(int(q[i][1]["offsets"][-1]) for q in panels[:r])
+                                       for r, p in enumerate(panels)])
+        assert (offs == g["offsets"]).all()
+        assert (np.concatenate([p[i][1]["col_indices"] for p in panels]) == g["col_indices"]).all()
+        assert (np.concatenate([p[i][1]["a"] for p in panels]) == g["a"]).all()
+        assert all((p[i][1]["b"] == g["b"]).all() for p in panels)
+    # world = 1 is exactly the C2 configuration (the reference cell seed of M = 4096)
+    one = bench.c2_rank_cases(0, 1)
+    seed = O.cell_seed(0, ((bench.M, bench.N, bench.K), bench.V, 0.9, "L8-R8"))
+    g = O.build_sddmm_case(bench.M, bench.N, bench.K, bench.V, 0.9, 8, 8, seed)
+    assert (one[2][1]["col_indices"] == g["col_indices"]).all()
