@@ -317,7 +317,10 @@ def bench_c2(ctx, args, status):
                    torch.empty(nblk * V, dtype=torch.int32, device=dev)]
         foot = sum(t.numel() * t.element_size() for t in tensors)
         st, tens = _sddmm_structs(tensors, nblk, Nn)
+        pid = Nn.ctypes.c_int32(-1)
+        Nn.check(lib.mc_sddmm_path(st[0], st[1], st[2], Nn.ctypes.byref(pid)))
         probs.append(dict(s=s, p=p, copies=[st], tensors=[tens], nblk=nblk, ops=2 * V * K * nblk,
+                          kernel=Nn.SDDMM_PATHS[pid.value],
                           bytes=sddmm_bytes(nblk), foot=foot, c=c))
     # cold-L2 discipline: enough device copies per problem that one rotation touches more
     # than COLD_BYTES (> 2x the 126 MB L2): no launch finds its operands in L2 from an
@@ -778,8 +781,7 @@ def run_ours(args):
         "hbm_gbs": pr["bytes"] / (c2["per_launch"][j] * 1e-3) / 1e9,
         "roofline_frac": (pr["bytes"] / (c2["per_launch"][j] * 1e-3) / 1e9) / hbm,
         "copies": pr["ncopy"],
-        "kernel": ("sddmm_tc_kernel (tcgen05 kind::i8 dense tile)" if pr["nblk"] * V / (M * N) >= 0.08
-                   else "sddmm_kernel (mma.sync gather)"),
+        "kernel": pr["kernel"],
     } for j, pr in enumerate(probs)}
     e2e = run_e2e(ctx, args, probs, c2["fault"])
 

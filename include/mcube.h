@@ -146,6 +146,15 @@ int mc_spmm_batched(const mc_srbcrs* lhs, int64_t lhs_words_stride,
 int mc_sddmm(const mc_dense* a, const mc_dense* b, const mc_bcrs* pattern,
              int32_t* out_values, uint32_t* status, void* stream);
 
+/* Which SDDMM kernel mc_sddmm / mc_sddmm_batched run for this problem (for reports and
+ * profiling; no launch). */
+enum {
+  MC_SDDMM_PATH_DENSE = 1,   /* sddmm_tc.cu: dense 128-column tiles on tcgen05 kind::i8     */
+  MC_SDDMM_PATH_GATHER8 = 2, /* sddmm.cu: pipelined 8-bit mma.sync gather (sparse patterns)  */
+  MC_SDDMM_PATH_GATHER = 3   /* sddmm.cu: generic mma.sync gather (16/4-bit, fp16 epilogue) */
+};
+int mc_sddmm_path(const mc_dense* a, const mc_dense* b, const mc_bcrs* pattern, int32_t* path);
+
 int mc_sddmm_batched(const mc_dense* a, int64_t a_words_stride,
                      const mc_dense* b, int64_t b_words_stride,
                      const mc_bcrs* pattern, int32_t batch,

@@ -36,6 +36,9 @@ SPMM_PATHS = {0: "spmm_kernel (mma.sync gather, 64-column tasks)",
               2: "densify + gemm_tc_kernel (tcgen05)",
               3: "spmm_tc_kernel (tcgen05 gather)",
               4: "spmm_kernel (per-nibble chunk products)"}
+SDDMM_PATHS = {1: "sddmm_tc_kernel (tcgen05 kind::i8 dense tile)",
+               2: "sddmm_g8_kernel (pipelined mma.sync gather)",
+               3: "sddmm_kernel (mma.sync gather)"}
 
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -84,6 +87,8 @@ _SIGNATURES = {
                           ctypes.c_size_t, _p]),
     "mc_spmm_batched": (_i32, [ctypes.POINTER(McSrBcrs), _i64, ctypes.POINTER(McDense), _i64, _i32,
                                ctypes.POINTER(McEpilogue), _p, _i64, _p, _p]),
+    "mc_sddmm_path": (_i32, [ctypes.POINTER(McDense), ctypes.POINTER(McDense), ctypes.POINTER(McBcrs),
+                             ctypes.POINTER(_i32)]),
     "mc_sddmm": (_i32, [ctypes.POINTER(McDense), ctypes.POINTER(McDense), ctypes.POINTER(McBcrs),
                         _p, _p, _p]),
     "mc_sddmm_batched": (_i32, [ctypes.POINTER(McDense), _i64, ctypes.POINTER(McDense), _i64,

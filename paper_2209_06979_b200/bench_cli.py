@@ -276,6 +276,15 @@ def _spmm_kernel_name(p) -> str:
     return N.SPMM_PATHS[pid.value]
 
 
+def _sddmm_kernel_name(p) -> str:
+    a, _k1 = D.dense_struct(p.a)
+    b, _k2 = D.dense_struct(p.b)
+    pat, _k3 = D.bcrs_struct(p.out_pattern)
+    pid = N.ctypes.c_int32(-1)
+    N.check(N.lib().mc_sddmm_path(a, b, pat, N.ctypes.byref(pid)))
+    return N.SDDMM_PATHS[pid.value]
+
+
 def run_sweep(spec: SweepSpec, verify_cells: bool = True) -> List[BenchRecord]:
     """bench.run_sweep (bench.py:193-207): every cell in stable order."""
     records: List[BenchRecord] = []
@@ -317,9 +326,7 @@ def _run_cell(spec: SweepSpec, shape, v, sparsity, precision, verify_cells) -> B
             out = t.empty(problem.out_pattern.n_blocks * v, dtype=t.int32, device="cuda")
             device = lambda: kernels.sddmm_device(problem, out=out, check_status=False)
             ops = 2 * v * rec.k * problem.out_pattern.n_blocks
-            dens = problem.out_pattern.n_blocks * v / max(1, rec.m * rec.n)
-            rec.kernel = ("sddmm_tc_kernel (tcgen05 dense tile)" if (lb, rb) == (8, 8) and dens >= 0.08
-                          and rec.k in (128, 256) else "sddmm_kernel (mma.sync gather)")
+            rec.kernel = _sddmm_kernel_name(problem)
         elif spec.op == "attention":
             cfg, (q, k, vmat) = _build_attention(spec, shape, v, sparsity, lb, rb, seed)
             runner = lambda: attention.sparse_attention(q, k, vmat, cfg)

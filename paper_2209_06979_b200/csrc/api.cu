@@ -208,11 +208,9 @@ int mc_spmm_ws(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n, int32_t*
   return cuda_status(launch_spmm(p, s), "mc_spmm_ws");
 }
 
-int mc_sddmm_batched(const mc_dense* a, int64_t a_words_stride, const mc_dense* b, int64_t b_words_stride,
-                     const mc_bcrs* pattern, int32_t batch, const mc_epilogue* epi, int32_t* out_values,
-                     int64_t out_stride, uint32_t* status, void* stream) {
-  int rc = check_sddmm(a, b, pattern);
-  if (rc) return rc;
+static SddmmParams sddmm_params(const mc_dense* a, int64_t a_words_stride, const mc_dense* b, int64_t b_words_stride,
+                                const mc_bcrs* pattern, int32_t batch, const mc_epilogue* epi, int32_t* out_values,
+                                int64_t out_stride, uint32_t* status) {
   SddmmParams p{};
   p.M = a->rows;
   p.K = a->cols;
@@ -238,8 +236,27 @@ int mc_sddmm_batched(const mc_dense* a, int64_t a_words_stride, const mc_dense* 
     p.f16_stride = epi->out_f16_batch_stride;
   }
   p.status = status;
+  return p;
+}
+
+int mc_sddmm_batched(const mc_dense* a, int64_t a_words_stride, const mc_dense* b, int64_t b_words_stride,
+                     const mc_bcrs* pattern, int32_t batch, const mc_epilogue* epi, int32_t* out_values,
+                     int64_t out_stride, uint32_t* status, void* stream) {
+  int rc = check_sddmm(a, b, pattern);
+  if (rc) return rc;
+  const SddmmParams p =
+      sddmm_params(a, a_words_stride, b, b_words_stride, pattern, batch, epi, out_values, out_stride, status);
   if (p.n_blocks == 0 || batch == 0) return MC_OK;
   return cuda_status(launch_sddmm(p, static_cast<cudaStream_t>(stream)), "mc_sddmm");
+}
+
+int mc_sddmm_path(const mc_dense* a, const mc_dense* b, const mc_bcrs* pattern, int32_t* path) {
+  int rc = check_sddmm(a, b, pattern);
+  if (rc) return rc;
+  if (!path) return fail(MC_ERR_VALUE, "path must not be NULL");
+  // a 256-byte aligned stand-in output: only the problem's shape and operands decide
+  *path = sddmm_path(sddmm_params(a, 0, b, 0, pattern, 1, nullptr, reinterpret_cast<int32_t*>(256), 0, nullptr));
+  return MC_OK;
 }
 
 int mc_sddmm(const mc_dense* a, const mc_dense* b, const mc_bcrs* pattern, int32_t* out_values, uint32_t* status,

@@ -87,6 +87,8 @@ cudaError_t launch_spmm_seg(const SpmmParams& p, cudaStream_t stream);
 bool spmm_tc_supported(const SpmmParams& p);
 cudaError_t launch_spmm_tc(SpmmParams p, cudaStream_t stream);
 cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream);
+// MC_SDDMM_PATH_* of the kernel launch_sddmm picks
+int sddmm_path(const SddmmParams& p);
 // dense-tile tcgen05 path (sddmm_tc.cu); launch_sddmm dispatches to it by density
 bool sddmm_tc_supported(const SddmmParams& p);
 cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream);

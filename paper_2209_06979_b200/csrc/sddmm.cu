@@ -20,6 +20,10 @@ namespace {
 
 constexpr int kWarps = 4;
 
+__device__ __forceinline__ void tc_prefetch_l2(const void* ptr) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
+
 // 16 consecutive k values of one operand row -> 4 int8-chunk words per chunk.
 template <int BITS, bool ALIGNED>
 __device__ __forceinline__ void load_k16(const uint32_t* __restrict__ words, int64_t row, int64_t K,
@@ -219,6 +223,143 @@ sddmm_kernel(const SddmmParams p) {
   if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
 }
 
+// 8-bit x 8-bit gather SDDMM for sparse patterns (C2 at <= 10 % density), software-
+// pipelined across groups of 16 blocks: while group j's MMAs run, the B^T rows of group j+1
+// are already in flight (two register buffers), and the column indices of the next two
+// groups are loaded one pair ahead. A warp task is a run of `p.splits`-th of a vector row's
+// groups; its V rows of A (K bytes each, the MMA B operand) are loaded once per task. Each
+// lane loads 16 contiguous bytes [64 s + 16 t, +16) of its two gathered rows per 64-byte
+// K chunk s; the reduction order inside a chunk is permuted identically for both operands
+// (MMA k-step (s, half) = bytes 64 s + 16 t + 8 half + 0..7), which leaves the int32 sums
+// exact. Stores: two 8-byte stores per lane, 256 contiguous bytes per warp instruction.
+// int8 products cannot overflow int32 for K <= 33025 (emulation.py:108-113, checked on the
+// host), so no overflow test is needed.
+template <int V, int KS>
+__global__ void __launch_bounds__(kWarps * 32)
+sddmm_g8_kernel(const SddmmParams p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  constexpr int K = 64 * KS;
+  const int64_t task = static_cast<int64_t>(blockIdx.x) * kWarps + warp;
+  const int64_t per_batch = p.vrows * p.splits;
+  const int64_t b = task / per_batch;
+  const int64_t rem = task - b * per_batch;
+  const int64_t r = rem / p.splits;
+  const int split = static_cast<int>(rem - r * p.splits);
+  // Uniform-row guess of this task's first blocks (exact for the reference generator's
+  // patterns): its column indices are loaded together with the row offsets instead of
+  // after them, and discarded if the offsets disagree. Before pdl_wait only L2 prefetches
+  // are issued (L2 is the coherence point: they cannot make a later read stale).
+  const int64_t lo_g = (r * p.n_blocks) / p.vrows, hi_g = ((r + 1) * p.n_blocks) / p.vrows;
+  const int64_t ng_g = (hi_g - lo_g + 15) >> 4;
+  const int64_t gb_g = (ng_g * split) / p.splits;
+  const uint8_t* __restrict__ Ar = reinterpret_cast<const uint8_t*>(p.a_words + b * p.a_stride) +
+                                   (r * V + (g < V ? g : 0)) * static_cast<int64_t>(K) + 16 * t;
+  if (task < p.tasks) {
+    if (lane == 0) tc_prefetch_l2(p.row_offsets + r);
+    if (lane < 2 && lo_g + gb_g * 16 < p.n_blocks) tc_prefetch_l2(p.col_indices + lo_g + gb_g * 16 + 16 * lane);
+    if (t == 0 && g < V) tc_prefetch_l2(Ar);
+  }
+  if (threadIdx.x == 0) pdl_launch_dependents();
+  pdl_wait();
+  if (task >= p.tasks) return;
+  const int64_t q_g = gb_g * 16 + lane;
+  const uint32_t spec = q_g < hi_g - lo_g ? __ldg(p.col_indices + lo_g + q_g) : 0u;
+  uint4 af[KS];
+#pragma unroll
+  for (int s = 0; s < KS; ++s)
+    af[s] = g < V ? __ldg(reinterpret_cast<const uint4*>(Ar + 64 * s)) : make_uint4(0u, 0u, 0u, 0u);
+  const int64_t lo = p.row_offsets[r], hi = p.row_offsets[r + 1];
+  const int64_t nb = hi - lo;
+  const int64_t ngroups = (nb + 15) >> 4;
+  const int64_t gbeg = (ngroups * split) / p.splits, gend = (ngroups * (split + 1)) / p.splits;
+  if (gbeg >= gend) return;
+  const uint32_t* __restrict__ cols = p.col_indices + lo;
+  const uint8_t* __restrict__ Bt = reinterpret_cast<const uint8_t*>(p.b_words + b * p.b_stride) + 16 * t;
+  int32_t* __restrict__ out = p.out + b * p.out_stride + lo * V;
+  const uint32_t ncols = static_cast<uint32_t>(p.N);
+
+  // columns of blocks [q0, q0 + 32) of the row (0 past the end; out-of-range ones flagged)
+  auto check = [&](int64_t q, uint32_t c) -> uint32_t {
+    if (q >= nb) return 0u;
+    if (c >= ncols) {
+      flag_status(p.status, MC_STATUS_BAD_INDEX);
+      return 0u;
+    }
+    return c;
+  };
+  auto colload = [&](int64_t q0) -> uint32_t {
+    const int64_t q = q0 + lane;
+    return check(q, q < nb ? __ldg(cols + q) : 0u);
+  };
+
+  // the two gathered rows (blocks g and g + 8 of the group in half `h` of colreg)
+  auto load = [&](uint32_t colreg, int h, uint4 (&xa)[KS], uint4 (&xb)[KS]) {
+    const uint32_t c_lo = __shfl_sync(0xffffffffu, colreg, 16 * h + g);
+    const uint32_t c_hi = __shfl_sync(0xffffffffu, colreg, 16 * h + g + 8);
+    const uint8_t* ra = Bt + static_cast<size_t>(c_lo) * K;
+    const uint8_t* rb = Bt + static_cast<size_t>(c_hi) * K;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      xa[s] = __ldg(reinterpret_cast<const uint4*>(ra + 64 * s));
+      xb[s] = __ldg(reinterpret_cast<const uint4*>(rb + 64 * s));
+    }
+  };
+  auto compute_store = [&](int64_t gi, const uint4 (&xa)[KS], const uint4 (&xb)[KS]) {
+    int acc[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      mma16832<false, false>(acc, xa[s].x, xb[s].x, xa[s].y, xb[s].y, af[s].x, af[s].y);
+      mma16832<false, false>(acc, xa[s].z, xb[s].z, xa[s].w, xb[s].w, af[s].z, af[s].w);
+    }
+    const int64_t blk0 = gi * 16;
+    const int64_t nvalid = nb - blk0;
+    if (2 * t < V) {
+      if (g < nvalid) *reinterpret_cast<int2*>(out + (blk0 + g) * V + 2 * t) = make_int2(acc[0], acc[1]);
+      if (g + 8 < nvalid) *reinterpret_cast<int2*>(out + (blk0 + g + 8) * V + 2 * t) = make_int2(acc[2], acc[3]);
+    }
+  };
+
+  uint4 fa[KS], fb[KS], ga[KS], gb[KS];
+  const bool spec_ok = lo == lo_g && hi == hi_g;  // then gbeg == gb_g and spec holds its columns
+  uint32_t colreg = spec_ok ? check(gbeg * 16 + lane, spec) : colload(gbeg * 16);
+  load(colreg, 0, fa, fb);
+  for (int64_t gi = gbeg; gi < gend; gi += 2) {
+    const bool has1 = gi + 1 < gend, has2 = gi + 2 < gend;
+    if (has1) load(colreg, 1, ga, gb);
+    const uint32_t colnext = has2 ? colload((gi + 2) * 16) : 0u;
+    compute_store(gi, fa, fb);
+    if (has2) load(colnext, 0, fa, fb);
+    if (has1) compute_store(gi + 1, ga, gb);
+    colreg = colnext;
+  }
+}
+
+// the pipelined 8-bit kernel takes int32 output, 8-bit operands, V in {4, 8} and
+// K a multiple of 64 up to 256 with 16-byte aligned rows
+bool sddmm_g8_supported(const SddmmParams& p) {
+  return p.LB == 8 && p.RB == 8 && (p.V == 4 || p.V == 8) && p.out != nullptr && p.out_f16 == nullptr &&
+         p.K > 0 && p.K % 64 == 0 && p.K <= 256 && (reinterpret_cast<uintptr_t>(p.a_words) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(p.b_words) & 15) == 0 && (reinterpret_cast<uintptr_t>(p.out) & 7) == 0 &&
+         (p.a_stride * 4) % 16 == 0 && (p.b_stride * 4) % 16 == 0 && (p.out_stride % 2) == 0 &&
+         !getenv("MCUBE_SDDMM_G8_OFF");
+}
+
+template <int V>
+cudaError_t launch_g8_v(const SddmmParams& p, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>((p.tasks + kWarps - 1) / kWarps);
+  if (grid == 0) return cudaSuccess;
+  cudaError_t e;
+  switch (p.K / 64) {
+    case 1: e = launch_pdl(sddmm_g8_kernel<V, 1>, dim3(grid), dim3(kWarps * 32), 0, s, p); break;
+    case 2: e = launch_pdl(sddmm_g8_kernel<V, 2>, dim3(grid), dim3(kWarps * 32), 0, s, p); break;
+    case 3: e = launch_pdl(sddmm_g8_kernel<V, 3>, dim3(grid), dim3(kWarps * 32), 0, s, p); break;
+    default: e = launch_pdl(sddmm_g8_kernel<V, 4>, dim3(grid), dim3(kWarps * 32), 0, s, p); break;
+  }
+  count_launch();
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 template <int LB, int RB, int V>
 cudaError_t launch_v(const SddmmParams& p, cudaStream_t s) {
   const bool aligned = ((p.K * LB) % 128 == 0) && ((p.K * RB) % 128 == 0) &&
@@ -265,14 +406,47 @@ static int sddmm_path_override() {
   return 0;
 }
 
-cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream) {
+// which kernel launch_sddmm runs (MC_SDDMM_PATH_*)
+int sddmm_path(const SddmmParams& p) {
   const int ov = sddmm_path_override();
   const double density = (p.M > 0 && p.N > 0) ? static_cast<double>(p.n_blocks) * p.V / (static_cast<double>(p.M) * p.N) : 0.0;
-  // K = 64 (attention heads, d = 64) stays on the gather kernel by default: with only two
+  // K = 64 (attention heads, d = 64) stays on a gather kernel by default: with only two
   // K-steps per tile the dense path is bound by draining the whole accumulator tile.
-  if (ov != 2 && sddmm_tc_supported(p) && (ov == 1 || (density >= 0.08 && p.K >= 128))) return launch_sddmm_tc(p, stream);
+  // Dense tile above a block density of 0.08 (the 16-bit / 4-bit gather kernel) or 0.15
+  // (the pipelined 8-bit gather kernel; C2 90 %: 8.1 us gather vs 12.0 us dense tile).
+  const bool g8 = sddmm_g8_supported(p);
+  double dense_min = g8 ? 0.15 : 0.08;
+  if (const char* e = getenv("MCUBE_SDDMM_DENSE_MIN")) dense_min = atof(e);
+  if (ov != 2 && sddmm_tc_supported(p) && (ov == 1 || (density >= dense_min && p.K >= 128))) return MC_SDDMM_PATH_DENSE;
+  return g8 ? MC_SDDMM_PATH_GATHER8 : MC_SDDMM_PATH_GATHER;
+}
+
+cudaError_t launch_sddmm(SddmmParams p, cudaStream_t stream) {
+  const int path = sddmm_path(p);
+  if (path == MC_SDDMM_PATH_DENSE) return launch_sddmm_tc(p, stream);
   // warps per vector row: about one group of 16 blocks each
   const double avg_groups = p.vrows ? (static_cast<double>(p.n_blocks) / p.vrows) / 16.0 : 0.0;
+  if (path == MC_SDDMM_PATH_GATHER8) {
+    // pipelined 8-bit kernel: as many warps per vector row as fit one wave of resident
+    // warps (measured on C2 90/95/98 %: a second partial wave costs more than the longer
+    // per-warp group runs; 4 warps per row there: 8.1 / 5.8 / ~4.8 us)
+    static int wave_warps = 0;
+    if (!wave_warps) {
+      int dev = 0, sms = 148, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sddmm_g8_kernel<8, 4>, kWarps * 32, 0);
+      wave_warps = sms * (per_sm > 0 ? per_sm : 1) * kWarps;
+    }
+    const int64_t rows = static_cast<int64_t>(p.batch) * p.vrows;
+    int64_t splits = rows > 0 ? wave_warps / rows : 1;
+    const int64_t max_groups = static_cast<int64_t>(avg_groups + 0.999);
+    if (splits > max_groups) splits = max_groups;
+    if (const char* e = getenv("MCUBE_SDDMM_SPLITS")) splits = atoi(e);
+    p.splits = static_cast<int>(splits < 1 ? 1 : (splits > 256 ? 256 : splits));
+    p.tasks = rows * p.splits;
+    return p.V == 8 ? launch_g8_v<8>(p, stream) : launch_g8_v<4>(p, stream);
+  }
   // groups of 16 blocks per warp: 1, or 2 when one group per warp would need more than
   // one wave of resident warps (C2 95 %: 1.6 waves -> 0.86; 10.2 -> 8.9 us, same-box A/B)
   double gpw = 1.0;

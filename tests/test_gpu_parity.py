@@ -616,3 +616,89 @@ def test_attention_fused_irregular_mask_rows(mode):
         assert (got[:8] == 0).all()  # vector row 0 is empty
         err = float(np.abs(got - ref["output"]).max())
         assert err <= (0.0 if mode == "parity" else mc.attention.FAST_MODE_TOLERANCE), (h, err)
+
+
+# ---------------- pipelined 8-bit gather SDDMM (sddmm_g8_kernel) ----------------
+
+def _sddmm_path_id(a, b, pat):
+    from paper_2209_06979_b200 import _device as D
+    from paper_2209_06979_b200 import _native as Nn
+    ad, _k1 = D.dense_struct(a)
+    bd, _k2 = D.dense_struct(b)
+    pd, _k3 = D.bcrs_struct(pat)
+    pid = Nn.ctypes.c_int32(-1)
+    Nn.check(Nn.lib().mc_sddmm_path(ad, bd, pd, Nn.ctypes.byref(pid)))
+    return pid.value
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("splits", ["1", "2", "3", "5"])
+@pytest.mark.parametrize("v", [4, 8])
+@pytest.mark.parametrize("k", [64, 128, 192, 256])
+def test_sddmm_g8_irregular_rows_vs_oracle(splits, v, k, monkeypatch):
+    """Pipelined 8-bit gather kernel on irregular rows (empty, full, clustered, random), with
+    1-5 warps per vector row (odd / even group counts per warp, pairs and single tails)."""
+    monkeypatch.setenv("MCUBE_SDDMM_PATH", "gather")
+    monkeypatch.setenv("MCUBE_SDDMM_SPLITS", splits)
+    m, n = 384, 1100
+    rng = np.random.default_rng(k + v + int(splits))
+    offs, cols = _irregular_pattern(m, n, v, 5 + k + v)
+    a = rng.integers(-128, 128, size=(m, k))
+    b = rng.integers(-128, 128, size=(k, n))
+    pat = mc.BcrsMatrix(m, n, v, offs, cols, mc.PackedArray.from_values(np.ones(cols.size * v), 8))
+    pa, pb = mc.pack_dense(a, 8, ROW_MAJOR), mc.pack_dense(b, 8, COL_MAJOR)
+    assert _sddmm_path_id(pa, pb, pat) == 2
+    out = mc.sddmm(mc.SddmmProblem(pa, pb, pat))
+    assert (np.asarray(out.values) == O.sddmm(a, b, offs, cols, v, 8, 8)).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sparsity", [0.9, 0.95, 0.98])
+def test_sddmm_c2_sparse_cells_default_path_all_rows(sparsity):
+    """C2 cells at 90/95/98 % on the default dispatch (the pipelined gather kernel), all rows."""
+    s = O.build_sddmm_case(4096, 4096, 256, 8, sparsity, 8, 8, seed=13)
+    pat = mc.BcrsMatrix(4096, 4096, 8, s["offsets"], s["col_indices"],
+                        mc.PackedArray.from_values(np.ones(s["col_indices"].size * 8), 8))
+    pa, pb = mc.pack_dense(s["a"], 8, ROW_MAJOR), mc.pack_dense(s["b"], 8, COL_MAJOR)
+    assert _sddmm_path_id(pa, pb, pat) == 2
+    out = np.asarray(mc.sddmm(mc.SddmmProblem(pa, pb, pat)).values)
+    assert (out == O.sddmm(s["a"], s["b"], s["offsets"], s["col_indices"], 8, 8, 8)).all()
+
+
+@pytest.mark.gpu
+def test_sddmm_g8_batched_and_bad_index():
+    """mc_sddmm_batched through the pipelined gather kernel (3 items sharing one pattern),
+    then an out-of-range column index: flagged, reported as FormatError by mc_status_fetch."""
+    import torch
+    from paper_2209_06979_b200 import _native as Nn
+    m, n, k, v, batch = 256, 512, 128, 8, 3
+    s = O.build_sddmm_case(m, n, k, v, 0.95, 8, 8, seed=31)
+    offs, cols = s["offsets"], s["col_indices"].astype(np.uint32)
+    rng = np.random.default_rng(9)
+    a = rng.integers(-128, 128, size=(batch, m, k)).astype(np.int8)
+    bt = rng.integers(-128, 128, size=(batch, n, k)).astype(np.int8)
+    dev = torch.device("cuda", 0)
+    a_d = torch.from_numpy(a.reshape(-1).view(np.int32).copy()).to(dev)
+    b_d = torch.from_numpy(bt.reshape(-1).view(np.int32).copy()).to(dev)
+    o_d = torch.from_numpy(offs.astype(np.int64)).to(dev)
+    c_d = torch.from_numpy(cols.view(np.int32).copy()).to(dev)
+    nblk = cols.size
+    out = torch.zeros(batch * nblk * v, dtype=torch.int32, device=dev)
+    ad = Nn.McDense(m, k, 8, Nn.MC_ROW_MAJOR, Nn.ptr(a_d))
+    bd = Nn.McDense(k, n, 8, Nn.MC_COL_MAJOR, Nn.ptr(b_d))
+    pd = Nn.McBcrs(m, n, v, 0, nblk, Nn.ptr(o_d), Nn.ptr(c_d))
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = Nn.lib()
+    pid = Nn.ctypes.c_int32(-1)
+    Nn.check(lib.mc_sddmm_path(ad, bd, pd, Nn.ctypes.byref(pid)))
+    assert pid.value == 2
+    Nn.check(lib.mc_sddmm_batched(ad, m * k // 4, bd, n * k // 4, pd, batch, None, Nn.ptr(out), nblk * v,
+                                  Nn.ptr(status), Nn.stream_ptr()))
+    Nn.check(lib.mc_status_fetch(Nn.ptr(status), Nn.stream_ptr()))
+    got = out.view(batch, -1).cpu().numpy()
+    for i in range(batch):
+        assert (got[i] == O.sddmm(a[i].astype(np.int64), bt[i].T.astype(np.int64), offs, cols, v, 8, 8)).all(), i
+    c_d[nblk // 2] = n + 7  # out of range
+    Nn.check(lib.mc_sddmm(ad, bd, pd, Nn.ptr(out), Nn.ptr(status), Nn.stream_ptr()))
+    with pytest.raises(mc.FormatError):
+        Nn.check(lib.mc_status_fetch(Nn.ptr(status), Nn.stream_ptr()))
