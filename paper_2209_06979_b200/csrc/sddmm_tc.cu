@@ -61,11 +61,6 @@ constexpr int kConsWarps = 8;
 constexpr int kFirstBuild = 2;
 constexpr int kFirstCons = kFirstBuild + kBuildWarps;
 constexpr int kThreads = 32 * (kFirstCons + kConsWarps);
-constexpr int kRowsPerBuilder = 32 / kBuildWarps;       // vector rows per builder warp
-constexpr int kLanesPerRow = 32 / kRowsPerBuilder;      // builder lanes per vector row
-#ifndef MCUBE_BUILDER_LDS128
-#define MCUBE_BUILDER_LDS128 0  // A/B: one LDS.128 of 4 consecutive candidates per lane
-#endif
 constexpr int kRingStride = 516;  // uint32 per row ring (512 + 4 pad)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -169,6 +164,8 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   constexpr int kStages = L::STAGES;
   constexpr int VR = L::VR;
   constexpr int PANEL = L::PANEL;
+  constexpr int kRowsPerBuilder = 32 / kBuildWarps;  // vector rows per builder warp
+  constexpr int kLanesPerRow = 32 / kRowsPerBuilder;  // builder lanes per vector row
   constexpr int kBW = VR / kRowsPerBuilder;  // active builder warps (the rest idle when VR = 16)
   constexpr uint32_t kIdesc = tc::idesc_i8(128, PANEL);
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -413,8 +410,9 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (t + 1 == t1 || tc_.ct + 1 == p.n_ctiles) tc::mma_commit(a_empty);  // panel's last tile
       }
     }
-  } else if (warp < kFirstBuild + kBW) {
-    // ---------------- pattern builders (4 independent warps) ----------------
+  } else {
+  if (warp < kFirstBuild + kBW) {
+    // ---------------- pattern builders (independent warps) ----------------
     // Builder warp bw owns vector rows 4*bw .. 4*bw+3 of the tile; lane = (row j, sub s),
     // eight lanes per row. Each row streams its CSR column list through a 512-entry ring
     // in shared memory (64-entry chunks, absolute position x in slot x & 511), fetched by
@@ -525,27 +523,14 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           landed = mtop_last = mtop;
         }
       }
-      // 32 candidates of each row per step, 4 consecutive ones per lane (one LDS.128 from a
-      // 16-byte aligned ring position: the up to 3 entries before the cursor have columns
-      // below c0 and are skipped); a step continues while any row of the warp still had a
-      // candidate inside the tile (columns strictly increasing) -- one vote per step
-#if MCUBE_BUILDER_LDS128
-      const int skew = (lo511 + cur) & 3;
-      const int abase = (lo511 + cur) - skew;
-      for (int k0 = 0; k0 < kCols + 4; k0 += 4 * kLanesPerRow) {
-        const int kb = k0 + 4 * sub;  // first candidate of this lane, relative to abase
-        const uint4 q4 = *reinterpret_cast<const uint4*>(rrow + ((abase + kb) & 511));
-        uint32_t c[4] = {q4.x, q4.y, q4.z, q4.w};
-        bool more = true;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = kb + u - skew;  // candidate index relative to the cursor
-          if (k < 0 || k >= lim) c[u] = (k < 0) ? c0 - 1u : kNone;  // before the cursor / past the window
-          const uint32_t off = c[u] - c0;
-          const bool in = off < static_cast<uint32_t>(kCols);
-          more &= (k < 0) || in;
-          bad |= in && c[u] >= static_cast<uint32_t>(p.N);
-#else
+      MC_STAMP(lane == 0 && bw == 0 && i < 5, 90 + static_cast<int>(i));
+      // candidates s, s + L, s + 2L, s + 3L of the step (L = lanes per row) per lane; a
+      // candidate outside the tile (off = c - c0 >= 128, kNone past the window) selects no
+      // bitmap word, so the routing is four predicated ORs (the loop is ALU-pipe bound). A
+      // step continues while some lane's last candidate was inside the tile (columns
+      // strictly increasing: then all its earlier ones were too) -- one vote per step.
+      // Out-of-range columns (>= N) can only fall inside the last column tile.
+      const bool last_ct = c0 + static_cast<uint32_t>(kCols) > static_cast<uint32_t>(p.N);
       for (int k0 = 0; k0 < kCols; k0 += 4 * kLanesPerRow) {
         uint32_t c[4];
 #pragma unroll
@@ -553,22 +538,24 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           const int k = k0 + sub + kLanesPerRow * u;
           c[u] = k < lim ? rrow[(lo511 + cur + k) & 511] : kNone;
         }
-        bool more = true;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const uint32_t off = c[u] - c0;
-          const bool in = off < static_cast<uint32_t>(kCols);
-          more &= in;
-          bad |= in && c[u] >= static_cast<uint32_t>(p.N);
-#endif
-          const uint32_t bit = in ? (1u << (off & 31)) : 0u;
-          const uint32_t wsel = off >> 5;
-          w0 |= wsel == 0 ? bit : 0u;
-          w1 |= wsel == 1 ? bit : 0u;
-          w2 |= wsel == 2 ? bit : 0u;
-          w3 |= wsel == 3 ? bit : 0u;
+          asm("{\n\t.reg .pred q;\n\t.reg .b32 t, ws;\n\t"
+              "shf.l.wrap.b32 t, 0, 1, %4;\n\t"  // 1 << (off & 31)
+              "shr.u32 ws, %4, 5;\n\t"
+              "setp.eq.u32 q, ws, 0;\n\t@q or.b32 %0, %0, t;\n\t"
+              "setp.eq.u32 q, ws, 1;\n\t@q or.b32 %1, %1, t;\n\t"
+              "setp.eq.u32 q, ws, 2;\n\t@q or.b32 %2, %2, t;\n\t"
+              "setp.eq.u32 q, ws, 3;\n\t@q or.b32 %3, %3, t;\n\t}"
+              : "+r"(w0), "+r"(w1), "+r"(w2), "+r"(w3)
+              : "r"(off));
         }
-        if (!__any_sync(0xffffffffu, more)) break;
+        if (last_ct) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) bad |= (c[u] - c0 < static_cast<uint32_t>(kCols)) && c[u] >= static_cast<uint32_t>(p.N);
+        }
+        if (!__any_sync(0xffffffffu, c[3] - c0 < static_cast<uint32_t>(kCols))) break;
       }
       MC_STAMP(lane == 0 && bw == 0 && i < 5, 65 + 5 * static_cast<int>(i));
       if (bad) flag_status(p.status, MC_STATUS_BAD_INDEX);
@@ -605,7 +592,8 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       MC_STAMP(lane == 0 && bw == 0 && i < 6, 22 + 3 * static_cast<int>(i));
     }
     cp_async_wait<0>();
-  } else if (warp >= kFirstCons) {
+  }
+  if (warp >= kFirstCons) {
     // ---------------- consumers: TMEM -> registers -> V*4-byte block stores ----------------
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = (warp - kFirstCons) >> 2;
@@ -688,6 +676,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       }
       MC_STAMP(warp == kFirstCons && lane == 0 && i < 6, 24 + 3 * static_cast<int>(i));
     }
+  }
   }
   tc::tc_fence_before();
   __syncthreads();

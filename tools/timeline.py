@@ -67,6 +67,8 @@ for i in range(5):
     names[65 + 5 * i] = f"b_loop{i}"
     names[66 + 5 * i] = f"b_red{i}"
     names[67 + 5 * i] = f"b_pempty{i}"
+for i in range(5):
+    names[90 + i] = f"b_land{i}"
 for cta in (0, 1, 77, 147):
     row = t[cta]
     ev = sorted((int(v - base), names.get(k, str(k))) for k, v in enumerate(row) if v >= base and v != 0)
