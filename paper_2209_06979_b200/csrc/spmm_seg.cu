@@ -49,7 +49,9 @@ struct SegCfg {
   static constexpr int A_STAGE = 2 * V * ABYTES;
   static constexpr int OFF_A = STAGES * kBStage;
   static constexpr int OFF_IDX = OFF_A + STAGES * A_STAGE;
-  static constexpr int WARP_BYTES = OFF_IDX + 5120;  // + 1 KB raw indices + 2 x 2 KB row addresses
+  // + 1 KB raw indices + 2 x 2 KB row addresses; 128-byte aligned (the consumer XORs chunk
+  // offsets into its row address)
+  static constexpr int WARP_BYTES = (OFF_IDX + 5120 + 127) / 128 * 128;
   static constexpr int SMEM = kW * WARP_BYTES + 1024;  // + alignment slack
 };
 
@@ -64,8 +66,25 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
       "l"(src), "r"(static_cast<int>(zero)));
 }
 
-// smem slot of MMA k = 16h + 4t + i
+// smem slot of MMA k = 16h + 4t + i: the k itself for the ldmatrix consumer (lane k of an
+// LDSM.x2 points at row k; rows 8j..8j+7 of a phase sit in 8 distinct 16-byte bank groups by
+// the c ^ (slot & 7) chunk swizzle); the PRMT consumer (MCUBE_SEG_PRMT) interleaves the rows
+// so that its per-lane LDS.128 are conflict-free
+#ifdef MCUBE_SEG_PRMT
 __device__ __forceinline__ constexpr int seg_slot(int h, int i, int t) { return 16 * h + 8 * (i >> 1) + 2 * t + (i & 1); }
+#else
+__device__ __forceinline__ constexpr int seg_slot(int h, int i, int t) { return 16 * h + 4 * t + i; }
+#endif
+
+// ldmatrix.m16n16.x2.trans.b8 (LDSM.8.MT1616.2): lanes 0-15 give the 16-byte rows k = 0..15
+// of matrix 0, lanes 16-31 rows k = 16..31 of matrix 1; lane (g, t) receives bytes (row k,
+// column g) / (k, g + 8) for k = 4t..4t+3 of matrix 0 in r0 / r1 and of matrix 1 in r2 / r3:
+// exactly the m16n8k32 A fragment of the 16 x 32 transpose (tools/micro/ldsm_probe.cu)
+__device__ __forceinline__ void ldsm_t16x2(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m16n16.x2.trans.shared.b8 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
 
 template <int LB, int RB, int V, int STAGES>
 __global__ void __launch_bounds__(kW * 32)
@@ -197,6 +216,147 @@ spmm_seg_kernel(const SpmmParams p) {
     cp_async_commit();
   };
 
+#ifndef MCUBE_SEG_PRMT
+  // ---- ldmatrix consumer. Chunk j (16 bytes) of the segment holds 16 byte-columns: 16 dense
+  // columns at 8 bits, 32 at 4 bits. One LDSM.x2 over the 32 gathered rows gives the A
+  // fragment of its 16 byte-columns x 32 k. 4-bit rows: a byte y = 16 hi + lo_u (hi signed, lo
+  // unsigned) enters two MMAs, y' = y ^ 0x08 per byte (= 16 hi + lo + 8 with lo the signed low
+  // nibble) and h = y & 0xF0 (= 16 hi):  odd column = acc(h) / 16 and even column =
+  // acc(y') - acc(h) - 8 sum_k a_k (the LHS sums: one DP4A per fragment word), all exact in
+  // int32 under spmm_seg_supported's |16 sum| bound -- 2 LOP per word, no transposes.
+  constexpr int NCH = kSeg / 16;            // 16-byte chunks per segment
+  constexpr int MM = RB == 4 ? 2 : 1;       // MMAs per chunk and LHS chunk
+  int acc[NCH][C::LC][MM][4];
+#pragma unroll
+  for (int j = 0; j < NCH; ++j)
+#pragma unroll
+    for (int c = 0; c < C::LC; ++c)
+#pragma unroll
+      for (int m = 0; m < MM; ++m)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[j][c][m][e] = 0;
+  int asum = 0;  // 4-bit RHS: this lane's share of sum_k a[v = g][k]
+  // lane's LDSM row: slot `lane`, chunk j at j ^ (lane & 7)
+  const uint32_t ldsm_off = static_cast<uint32_t>(lane * kSeg + ((lane & 7) << 4));
+
+  if (nsteps > 0) {
+    fetch_raw(0);
+    cp_async_commit();
+    convert(0, std::integral_constant<int, 0>());
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < nsteps) issue(s);
+      else cp_async_commit();
+    }
+  }
+  for (int s = 0; s < nsteps; ++s) {
+    const int nxt = s + STAGES - 1;
+    if (nxt < nsteps) issue(nxt);
+    else cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    const int st = s % STAGES;
+    __syncwarp();
+
+    const uint8_t* sa = wbuf + C::OFF_A + st * C::A_STAGE;
+    // ---- MMA B operand: LHS chunk words for k = 16h + 4t .. +3 of row v = g ----
+    uint32_t bf[C::LC][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gv = g < V ? g : 0;
+      const uint8_t* ar = sa + (S == 32 ? 2 * gv + h : h * V + gv) * C::ABYTES;
+      if constexpr (LB == 8) {
+        bf[0][h] = *reinterpret_cast<const uint32_t*>(ar + 4 * t);
+      } else if constexpr (LB == 4) {
+        bf[0][h] = unpack_s4x4_ordered(*reinterpret_cast<const uint16_t*>(ar + 2 * t));
+      } else {  // LB == 16
+        const uint2 w = *reinterpret_cast<const uint2*>(ar + 8 * t);
+        split16(w.x, w.y, bf[0][h], bf[1][h]);
+      }
+      if (g >= V) {
+#pragma unroll
+        for (int c = 0; c < C::LC; ++c) bf[c][h] = 0u;
+      }
+    }
+    if constexpr (RB == 4) {
+      asum = __dp4a(static_cast<int>(bf[0][0]), 0x01010101, asum);
+      asum = __dp4a(static_cast<int>(bf[0][1]), 0x01010101, asum);
+    }
+    const uint32_t row_addr = wbuf_s + st * kBStage + ldsm_off;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      uint32_t a[4];
+      ldsm_t16x2(row_addr ^ (j << 4), a[0], a[1], a[2], a[3]);
+      if constexpr (RB == 4) {
+        uint32_t y[4], hh[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          y[e] = a[e] ^ 0x08080808u;
+          hh[e] = a[e] & 0xF0F0F0F0u;
+        }
+        mma16832<false, false>(acc[j][0][0], y[0], y[1], y[2], y[3], bf[0][0], bf[0][1]);
+        mma16832<false, false>(acc[j][0][1], hh[0], hh[1], hh[2], hh[3], bf[0][0], bf[0][1]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < C::LC; ++c) {
+          if (LB == 16 && c == 0)
+            mma16832<false, true>(acc[j][c][0], a[0], a[1], a[2], a[3], bf[c][0], bf[c][1]);
+          else
+            mma16832<false, false>(acc[j][c][0], a[0], a[1], a[2], a[3], bf[c][0], bf[c][1]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  cp_async_wait<0>();  // a raw index chunk past the last step may still be in flight
+
+  // ---- epilogue: exact recombination + the reference's int32 checks. Lane (g, t) holds
+  // byte-columns g and g + 8 of every chunk for rows v = 2t, 2t + 1 ----
+  bool overflow = false;
+  const int64_t row0 = r * V;
+  int32_t* outb = p.out + b * p.out_stride;
+  long long vsum[2] = {0, 0};
+  if constexpr (RB == 4) {
+    asum += __shfl_xor_sync(0xffffffffu, asum, 1);
+    asum += __shfl_xor_sync(0xffffffffu, asum, 2);  // sum_k a[g][k] in every lane of group g
+    vsum[0] = __shfl_sync(0xffffffffu, asum, 8 * t);      // v = 2t
+    vsum[1] = __shfl_sync(0xffffffffu, asum, 8 * t + 4);  // v = 2t + 1
+  }
+#pragma unroll
+  for (int vv = 0; vv < 2; ++vv) {
+    const int v = 2 * t + vv;
+    if (v >= V) continue;
+    int32_t* o = outb + (row0 + v) * p.N;
+#pragma unroll
+    for (int j = 0; j < NCH; ++j)
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        const int e = 2 * hi + vv;
+        if constexpr (RB == 4) {
+          const long long hsum = acc[j][0][1][e];
+          const long long odd = hsum >> 4;
+          const long long even = static_cast<long long>(acc[j][0][0][e]) - hsum - 8 * vsum[vv];
+          overflow |= !fits_i32(even) || !fits_i32(odd);
+          const int64_t n = c0 + 32 * j + 16 * hi + 2 * g;
+          if (n < p.N) *reinterpret_cast<int2*>(o + n) = make_int2(static_cast<int32_t>(even), static_cast<int32_t>(odd));
+        } else {
+          long long total;
+          if constexpr (C::LC == 2) {
+            const long long lo = acc[j][0][0][e];
+            const long long hh = 256LL * acc[j][1][0][e];
+            if constexpr (V == 8) overflow |= !fits_i32(hh);
+            else overflow |= !fits_i32(lo + hh);
+            total = lo + hh;
+          } else {
+            total = acc[j][0][0][e];
+          }
+          overflow |= !fits_i32(total);
+          const int64_t n = c0 + 16 * j + 8 * hi + g;
+          if (n < p.N) o[n] = static_cast<int32_t>(total);
+        }
+      }
+  }
+#else
   int acc[NS][C::LC][4][4];
 #pragma unroll
   for (int s = 0; s < NS; ++s)
@@ -350,6 +510,7 @@ spmm_seg_kernel(const SpmmParams p) {
       }
     }
   }
+#endif
   if (overflow) flag_status(p.status, MC_STATUS_OVERFLOW);
   if (bad_idx) flag_status(p.status, MC_STATUS_BAD_INDEX);
 }
