@@ -178,7 +178,8 @@ int mc_spmm_workspace(const mc_srbcrs* lhs, const mc_dense* rhs, size_t* bytes) 
   if (!bytes) return fail(MC_ERR_VALUE, "bytes must not be NULL");
   // a placeholder output pointer: eligibility only looks at its alignment
   SpmmParams p = spmm_params(lhs, 0, rhs, 0, 1, nullptr, reinterpret_cast<int32_t*>(256), 0, nullptr);
-  *bytes = dense_spmm_workspace(p);
+  const size_t dense = dense_spmm_workspace(p);
+  *bytes = dense > 0 ? dense : spmm_seg_workspace(p);
   return MC_OK;
 }
 
@@ -205,6 +206,9 @@ int mc_spmm_ws(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n, int32_t*
   const size_t need = dense_spmm_workspace(p);
   if (workspace && need > 0 && workspace_bytes >= need)
     return cuda_status(launch_dense_spmm(p, workspace, s), "mc_spmm_ws");
+  const size_t seg = need > 0 ? 0 : spmm_seg_workspace(p);
+  if (workspace && seg > 0 && workspace_bytes >= seg)
+    return cuda_status(launch_spmm_seg_ws(p, workspace, s), "mc_spmm_ws");
   return cuda_status(launch_spmm(p, s), "mc_spmm_ws");
 }
 

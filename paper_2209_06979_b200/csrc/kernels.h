@@ -80,9 +80,12 @@ size_t dense_spmm_workspace(const SpmmParams& p);
 cudaError_t launch_dense_spmm(SpmmParams p, void* workspace, cudaStream_t stream);
 cudaError_t launch_gemm_tc(const SpmmParams& p, const int8_t* a0, const int8_t* a1, const int8_t* b0,
                            const int8_t* b1, cudaStream_t stream);
-// TMA gather4 path (spmm_seg.cu) for the large gather-bound problems
+// row-segment gather path (spmm_seg.cu) for the large gather-bound problems; with a
+// workspace (spmm_seg_workspace bytes) a 4-bit right-hand side is pre-transformed once
 bool spmm_seg_supported(const SpmmParams& p);
 cudaError_t launch_spmm_seg(const SpmmParams& p, cudaStream_t stream);
+size_t spmm_seg_workspace(const SpmmParams& p);
+cudaError_t launch_spmm_seg_ws(SpmmParams p, void* workspace, cudaStream_t stream);
 // tcgen05 gather path (spmm_tc.cu); launch_spmm dispatches to it when supported
 bool spmm_tc_supported(const SpmmParams& p);
 cudaError_t launch_spmm_tc(SpmmParams p, cudaStream_t stream);

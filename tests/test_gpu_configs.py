@@ -142,14 +142,19 @@ def test_attention_head_shards_equal_unsharded():
     assert torch.equal(torch.cat(parts), full)
 
 
+@pytest.mark.parametrize("prexor", ["1", "0"])
 @pytest.mark.parametrize("sparsity", [0.5, 0.95])
 @pytest.mark.parametrize("v", [2, 4, 8])
 @pytest.mark.parametrize("pair,n", [((8, 4), 512), ((8, 4), 96), ((4, 4), 256), ((8, 8), 384), ((8, 8), 48),
                                     ((16, 8), 256)])
-def test_spmm_segment_path_vs_oracle(pair, n, v, sparsity, monkeypatch):
-    """The TMA gather4 SpMM kernel (spmm_seg.cu, the C5 kernel) forced on small problems:
-    every V, ragged N (zero-filled segment tails), empty / irregular rows."""
+def test_spmm_segment_path_vs_oracle(pair, n, v, sparsity, prexor, monkeypatch):
+    """The row-segment SpMM kernel (spmm_seg.cu, the C5 kernel) forced on small problems:
+    every V, ragged N (zero-filled segment tails), empty / irregular rows; 4-bit right-hand
+    sides with the pre-XORed workspace copy (mc_spmm_ws) and without it."""
+    if prexor == "0" and pair[1] != 4:
+        pytest.skip("the workspace variant exists for 4-bit right-hand sides only")
     monkeypatch.setenv("MCUBE_SPMM_PATH", "seg")
+    monkeypatch.setenv("MCUBE_SEG_PREXOR", prexor)
     lb, rb = pair
     m, k = 256, 640
     c = O.build_spmm_case(m, n, k, v, sparsity, lb, rb, seed=lb + rb + v + n)
