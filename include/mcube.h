@@ -48,21 +48,15 @@ extern "C" {
 /* SR-BCRS matrix (sparse_format.py:129-230, SrBcrsMatrix).
  * Element (v, j) of stored stride s lives at s*V*stride + v*stride + j;
  * values are `bit_width`-bit two's complement packed LSB-first in uint32
- * words (qint.py:41-62). `shuffled` holds flags: MC_SRBCRS_SHUFFLED means
- * col_indices were permuted by SHUFFLE_PERMUTATION in blocks of 8
- * (sparse_format.py:373-385); MC_SRBCRS_SORTED is the caller's assertion that
- * every row's columns are non-decreasing in unshuffled order (true for any
- * SR-BCRS built from a BcrsMatrix, sparse_format.py:99-102), which lets the
- * dense-tile path build LHS tiles in shared memory without a densify pass. */
-#define MC_SRBCRS_SHUFFLED 1
-#define MC_SRBCRS_SORTED 2
+ * words (qint.py:41-62). shuffled != 0 means col_indices were permuted by
+ * SHUFFLE_PERMUTATION in blocks of 8 (sparse_format.py:373-385). */
 typedef struct mc_srbcrs {
   int64_t scalar_rows;          /* M                                   */
   int64_t scalar_cols;          /* K                                   */
   int32_t vector_length;        /* V in {2,4,8}                        */
   int32_t stride;               /* S, stored vectors per stride        */
   int32_t bit_width;            /* 4, 8, 12 or 16                      */
-  int32_t shuffled;             /* MC_SRBCRS_* flags (0/1 = shuffled)  */
+  int32_t shuffled;             /* 0/1                                 */
   int64_t stored_vectors;       /* length of col_indices               */
   const int64_t* row_begin;     /* [M/V] first stored vector of row    */
   const int64_t* row_end;       /* [M/V] one past the last valid one   */

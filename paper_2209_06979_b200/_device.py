@@ -93,50 +93,6 @@ def any_host(*objs) -> bool:
     return False
 
 
-_PERM = (0, 2, 4, 6, 1, 3, 5, 7)  # SHUFFLE_PERMUTATION (sparse_format.py:30)
-
-
-def rows_sorted(m) -> bool:
-    """True when every row's columns are non-decreasing over its valid positions, in
-    unshuffled order -- the invariant of any SR-BCRS built from a BcrsMatrix
-    (sparse_format.py:99-102) that the shared-memory LHS builder of the dense-tile SpMM
-    relies on (MC_SRBCRS_SORTED). Hand-built containers may violate it; they then take
-    the densify path. Vectorised, once per container (cached with its device copy)."""
-    t = torch()
-    n = int(m.col_indices.numel() if is_torch(m.col_indices) else np.asarray(m.col_indices).size)
-    if n < 2:
-        return True
-    if is_torch(m.col_indices) or is_torch(m.row_begin):
-        dev = m.col_indices.device if is_torch(m.col_indices) else t.device("cuda")
-        idx = (m.col_indices if is_torch(m.col_indices) else t.from_numpy(
-            np.asarray(m.col_indices, dtype=np.uint32).view(np.int32))).to(dev).view(t.int32).to(t.int64) & 0xFFFFFFFF
-        if m.shuffled:
-            blk = idx.view(-1, 8)
-            out = t.empty_like(blk)
-            out[:, list(_PERM)] = blk
-            idx = out.reshape(-1)
-        begin = t.as_tensor(m.row_begin, device=dev).to(t.int64)
-        end = t.as_tensor(m.row_end, device=dev).to(t.int64)
-        true = end - begin
-        stored = (true + m.stride - 1) // m.stride * m.stride
-        off = t.arange(n, device=dev) - t.repeat_interleave(begin, stored, output_size=n)
-        tr = t.repeat_interleave(true, stored, output_size=n)
-        pair = (off[:-1] + 1) < tr[:-1]
-        return bool(((idx[1:] >= idx[:-1]) | ~pair).all())
-    idx = np.asarray(m.col_indices, dtype=np.uint32).astype(np.int64)
-    if m.shuffled:
-        blk = idx.reshape(-1, 8)
-        out = np.empty_like(blk)
-        out[:, list(_PERM)] = blk
-        idx = out.reshape(-1)
-    begin = np.asarray(m.row_begin, dtype=np.int64)
-    true = np.asarray(m.row_end, dtype=np.int64) - begin
-    stored = (true + m.stride - 1) // m.stride * m.stride
-    off = np.arange(n, dtype=np.int64) - np.repeat(begin, stored)
-    pair = (off[:-1] + 1) < np.repeat(true, stored)[:-1]
-    return bool(np.all((idx[1:] >= idx[:-1]) | ~pair))
-
-
 def srbcrs_struct(m):
     def make():
         begin = to_dev(m.row_begin, np.int64)
@@ -144,9 +100,8 @@ def srbcrs_struct(m):
         idx = to_dev(m.col_indices, np.uint32)
         words = words_of(m.values)
         bits = getattr(m.values, "bit_width", 32)
-        flags = (N.MC_SRBCRS_SHUFFLED if m.shuffled else 0) | (N.MC_SRBCRS_SORTED if rows_sorted(m) else 0)
         s = N.McSrBcrs(m.scalar_rows, m.scalar_cols, m.vector_length, m.stride, bits,
-                       flags, int(idx.numel()), N.ptr(begin), N.ptr(end),
+                       int(bool(m.shuffled)), int(idx.numel()), N.ptr(begin), N.ptr(end),
                        N.ptr(idx), N.ptr(words))
         return s, (begin, end, idx, words)
     return cached(m, "srbcrs", make)

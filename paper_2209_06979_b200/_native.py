@@ -29,7 +29,6 @@ MC_ERR_CUDA = 6
 
 MC_ROW_MAJOR = 0
 MC_COL_MAJOR = 1
-MC_SRBCRS_SHUFFLED, MC_SRBCRS_SORTED = 1, 2  # mc_srbcrs.shuffled flags
 MC_DTYPE_F16, MC_DTYPE_F32, MC_DTYPE_F64 = 0, 1, 2
 MC_ATTN_PARITY, MC_ATTN_FAST = 0, 1
 SPMM_PATHS = {0: "spmm_kernel (mma.sync gather, 64-column tasks)",

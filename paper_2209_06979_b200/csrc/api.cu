@@ -61,9 +61,9 @@ static int check_spmm(const mc_srbcrs* a, const mc_dense* b, int bs_n) {
                 (long long)b->rows);
   if (!spmm_pair_ok(a->bit_width, b->bit_width))
     return fail(MC_ERR_UNSUPPORTED_PRECISION, "L%d-R%d is not supported for spmm", a->bit_width, b->bit_width);
-  if (b->bit_width == 4 && !(a->shuffled & MC_SRBCRS_SHUFFLED))
+  if (b->bit_width == 4 && !a->shuffled)
     return fail(MC_ERR_SHUFFLE_STATE, "4-bit RHS requires shuffled LHS column indices");
-  if (b->bit_width != 4 && (a->shuffled & MC_SRBCRS_SHUFFLED))
+  if (b->bit_width != 4 && a->shuffled)
     return fail(MC_ERR_SHUFFLE_STATE, "shuffled LHS indices are only valid with a 4-bit RHS");
   const int w = plan_width(a->bit_width, b->bit_width);
   const int tile_k = w == 8 ? 16 : 32;
@@ -133,8 +133,7 @@ static SpmmParams spmm_params(const mc_srbcrs* lhs, int64_t lhs_words_stride, co
   p.S = lhs->stride;
   p.LB = lhs->bit_width;
   p.RB = rhs->bit_width;
-  p.shuffled = (lhs->shuffled & MC_SRBCRS_SHUFFLED) ? 1 : 0;
-  p.sorted = (lhs->shuffled & MC_SRBCRS_SORTED) ? 1 : 0;
+  p.shuffled = lhs->shuffled;
   p.batch = batch;
   p.row_begin = lhs->row_begin;
   p.row_end = lhs->row_end;

@@ -9,8 +9,6 @@
 // the GEMM recombines chunk products in int64 with the reference's int32 checks.
 #include <cuda_fp16.h>
 
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.h"
 
@@ -201,19 +199,11 @@ bool densify_stride_ok(const SpmmParams& p) {
 int dense_lhs_planes(int lb) { return lb >= 12 ? 2 : 1; }
 int dense_rhs_planes(int rb) { return rb == 16 ? 2 : 1; }
 
-// The LHS goes straight from SR-BCRS into the GEMM's shared-memory operand (gemm_sp.cu)
-// when the rows are asserted sorted (gemm_sp_ok); otherwise, or with MCUBE_DENSIFY=1, the
-// two-pass densify_kernel + gemm_tc_kernel path runs.
-static bool use_densify(const SpmmParams& p) {
-  const char* e = getenv("MCUBE_DENSIFY");
-  return (e && e[0] == '1') || !gemm_sp_ok(p);
-}
-
-// Workspace of the dense path: RC planes of K x N int8 unless the RHS already is int8 (+ LC
-// planes of M x K int8 on the densify path). 0 when the problem is not eligible.
+// Workspace of the dense path: LC planes of M x K int8 (+ RC planes of K x N int8 unless
+// the RHS already is int8). 0 when the problem is not eligible.
 size_t dense_spmm_workspace(const SpmmParams& p) {
   if (!dense_spmm_eligible(p)) return 0;
-  const size_t a = use_densify(p) ? static_cast<size_t>(dense_lhs_planes(p.LB)) * p.M * p.K : 0;
+  const size_t a = static_cast<size_t>(dense_lhs_planes(p.LB)) * p.M * p.K;
   const size_t b = p.RB == 8 ? 0 : static_cast<size_t>(dense_rhs_planes(p.RB)) * p.K * p.N;
   return a + b + 1024;
 }
@@ -221,26 +211,6 @@ size_t dense_spmm_workspace(const SpmmParams& p) {
 cudaError_t launch_dense_spmm(SpmmParams p, void* workspace, cudaStream_t stream) {
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   ws += (1024 - (reinterpret_cast<uintptr_t>(ws) & 1023)) & 1023;
-  if (!use_densify(p)) {
-    const int8_t* b0 = reinterpret_cast<const int8_t*>(p.rhs_words);
-    const int8_t* b1 = nullptr;
-    if (p.RB != 8) {
-      const size_t plane_b = static_cast<size_t>(p.K) * p.N;
-      int8_t* w0 = reinterpret_cast<int8_t*>(ws);
-      int8_t* w1 = p.RB == 16 ? w0 + plane_b : nullptr;
-      const int64_t n16 = static_cast<int64_t>(plane_b / 16);
-      const unsigned grid = static_cast<unsigned>((n16 + 255) / 256);
-      if (p.RB == 4) widen_kernel<4><<<grid, 256, 0, stream>>>(p.rhs_words, n16, w0, w1);
-      else widen_kernel<16><<<grid, 256, 0, stream>>>(p.rhs_words, n16, w0, w1);
-      count_launch();
-      const cudaError_t e = cudaGetLastError();
-      if (e != cudaSuccess) return e;
-      b0 = w0;
-      b1 = w1;
-    }
-    if (const char* e = getenv("MCUBE_SP_PROBE")) p.gather_tma = atoi(e);  // variant-library timing probe
-    return launch_gemm_sp(p, b0, b1, stream);
-  }
   const size_t plane_a = static_cast<size_t>(p.M) * p.K;
   int8_t* a0 = reinterpret_cast<int8_t*>(ws);
   int8_t* a1 = dense_lhs_planes(p.LB) == 2 ? a0 + plane_a : nullptr;

@@ -11,7 +11,6 @@ void count_launch();
 struct SpmmParams {
   int64_t M, K, N, vrows;
   int V, S, LB, RB, shuffled, batch;
-  int sorted;  // caller asserts non-decreasing columns per row (MC_SRBCRS_SORTED)
   const int64_t* row_begin;
   const int64_t* row_end;
   const uint32_t* col_indices;
@@ -79,9 +78,6 @@ bool densify_stride_ok(const SpmmParams& p);
 // planes in a caller-provided workspace, then an exact tcgen05 GEMM
 bool dense_spmm_eligible(const SpmmParams& p);
 size_t dense_spmm_workspace(const SpmmParams& p);
-// SR-BCRS LHS built in shared memory inside the tcgen05 GEMM (gemm_sp.cu); b0/b1 = RHS int8 planes
-cudaError_t launch_gemm_sp(const SpmmParams& p, const int8_t* b0, const int8_t* b1, cudaStream_t stream);
-bool gemm_sp_ok(const SpmmParams& p);
 cudaError_t launch_dense_spmm(SpmmParams p, void* workspace, cudaStream_t stream);
 cudaError_t launch_gemm_tc(const SpmmParams& p, const int8_t* a0, const int8_t* a1, const int8_t* b0,
                            const int8_t* b1, cudaStream_t stream);

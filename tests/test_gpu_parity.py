@@ -424,16 +424,12 @@ def test_spmm_tc_irregular_rows(stride, gather, monkeypatch):
 
 # ---------------- dense-tile SpMM (densify + exact tcgen05 GEMM) vs the oracle ----------------
 
-@pytest.mark.parametrize("densify", ["0", "1"])
 @pytest.mark.parametrize("pair", PAIRS)
 @pytest.mark.parametrize("v", [2, 4, 8])
 @pytest.mark.parametrize("sparsity", [0.5, 0.9, 0.98])
-def test_spmm_dense_path_vs_oracle(pair, v, sparsity, densify, monkeypatch):
-    """Dense-tile SpMM: LHS tiles built in shared memory inside the GEMM (gemm_sp.cu) and the
-    two-pass densify + GEMM (MCUBE_DENSIFY=1)."""
+def test_spmm_dense_path_vs_oracle(pair, v, sparsity, monkeypatch):
     lb, rb = pair
     monkeypatch.setenv("MCUBE_SPMM_PATH", "dense")
-    monkeypatch.setenv("MCUBE_DENSIFY", densify)
     m, n, k = 256, 256, 512
     c = O.build_spmm_case(m, n, k, v, sparsity, lb, rb, seed=lb * 100 + rb + v + int(sparsity * 100))
     lhs = mc.SrBcrsMatrix(m, k, v, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
@@ -441,39 +437,6 @@ def test_spmm_dense_path_vs_oracle(pair, v, sparsity, densify, monkeypatch):
     out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], rb)))
     want = O.spmm(c["row_begin"], c["row_end"], c["col_indices"], c["values"], v, c["stride"],
                   c["shuffled"], lb, c["rhs"], rb, n)
-    assert (np.asarray(out) == want).all()
-
-
-@pytest.mark.parametrize("pair", [(8, 8), (16, 16), (16, 8), (4, 4)])
-def test_spmm_dense_path_unsorted_rows_take_densify(pair, monkeypatch):
-    """A hand-built SR-BCRS whose row columns are not increasing (the reference's spmm sums
-    any order) must not reach the shared-memory LHS builder, which assumes sorted rows: it
-    is detected on the host (MC_SRBCRS_SORTED unset) and runs through densify."""
-    from paper_2209_06979_b200 import _device as Dv
-    lb, rb = pair
-    monkeypatch.setenv("MCUBE_SPMM_PATH", "dense")
-    m, n, k, v = 256, 256, 512, 8
-    c = O.build_spmm_case(m, n, k, v, 0.7, lb, rb, seed=lb + rb)
-    idx = c["col_indices"].copy()
-    vals = c["values"].copy().reshape(-1, v, c["stride"])
-    # reverse the stored order inside the first stride block of every row (values with it)
-    s = c["stride"]
-    for r in range(m // v):
-        b0 = int(c["row_begin"][r])
-        n_true = int(c["row_end"][r] - b0)
-        if n_true >= s:
-            blk = b0 // s
-            if c["shuffled"]:
-                continue  # permuting shuffled blocks would need the shuffle undone first
-            idx[b0:b0 + s] = idx[b0:b0 + s][::-1]
-            vals[blk] = vals[blk][:, ::-1]
-    vals = vals.reshape(-1)
-    lhs = mc.SrBcrsMatrix(m, k, v, s, c["row_begin"], c["row_end"], idx,
-                          mc.PackedArray.from_values(vals, lb), shuffled=c["shuffled"])
-    if not c["shuffled"]:
-        assert not Dv.rows_sorted(lhs)
-    out = mc.spmm(mc.SpmmProblem(lhs, mc.pack_dense(c["rhs"], rb)))
-    want = O.spmm(c["row_begin"], c["row_end"], idx, vals, v, s, c["shuffled"], lb, c["rhs"], rb, n)
     assert (np.asarray(out) == want).all()
 
 

@@ -181,23 +181,3 @@ def test_compute_requires_cuda_no_fallback():
     rhs = mc.pack_dense(np.zeros((64, 32), dtype=np.int64), 8)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         mc.spmm(mc.SpmmProblem(lhs, rhs))
-
-
-def test_rows_sorted_flag_detects_hand_built_disorder():
-    """MC_SRBCRS_SORTED (the shared-memory LHS builder's precondition) is set for SR-BCRS built
-    from a BcrsMatrix and cleared for a hand-built container with a row out of order."""
-    from paper_2209_06979_b200 import _device as Dv
-    c = O.build_spmm_case(64, 64, 256, 8, 0.5, 8, 4, seed=5)
-    lhs = mc.SrBcrsMatrix(64, 256, 8, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
-                          mc.PackedArray.from_values(c["values"], 8), shuffled=c["shuffled"])
-    assert c["shuffled"] and Dv.rows_sorted(lhs)
-    c = O.build_spmm_case(64, 64, 256, 8, 0.5, 8, 8, seed=6)
-    ok = mc.SrBcrsMatrix(64, 256, 8, c["stride"], c["row_begin"], c["row_end"], c["col_indices"],
-                         mc.PackedArray.from_values(c["values"], 8))
-    assert Dv.rows_sorted(ok)
-    idx = c["col_indices"].copy()
-    b0, b1 = int(c["row_begin"][3]), int(c["row_end"][3])
-    idx[b0], idx[b1 - 1] = idx[b1 - 1], idx[b0]
-    bad = mc.SrBcrsMatrix(64, 256, 8, c["stride"], c["row_begin"], c["row_end"], idx,
-                          mc.PackedArray.from_values(c["values"], 8))
-    assert not Dv.rows_sorted(bad)
