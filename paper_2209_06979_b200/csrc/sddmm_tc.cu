@@ -630,6 +630,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
       uint32_t va[32], vb[32];
       tc::tmem_ld32_issue(tl, va);
       tc::tmem_wait_ld();
+      MC_STAMP(warp == kFirstCons && lane == 0 && i < 3, 110 + static_cast<int>(i));
       if (p.out_f16 == nullptr) {
         int32_t* out = p.out + item * p.out_stride;
 #pragma unroll
@@ -652,6 +653,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
           }
           if (kk + 1 < kChunks) tc::tmem_wait_ld();
         }
+        MC_STAMP(warp == kFirstCons && lane == 0 && i < 3, 113 + static_cast<int>(i));
       } else {
         // fused dequant epilogue (attention.py:147-154): fp16(acc * alpha) per block as one
         // V*2-byte store (+ the int32 accumulators when requested), rounded exactly as the
@@ -690,6 +692,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         tc::mbar_arrive(pempty_bar(slot));
       }
       MC_STAMP(warp == kFirstCons && lane == 0 && i < 6, 24 + 3 * static_cast<int>(i));
+      MC_STAMP(warp == kFirstCons + 7 && lane == 0 && i < 3, 116 + static_cast<int>(i));
     }
   }
   }

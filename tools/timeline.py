@@ -69,6 +69,10 @@ for i in range(5):
     names[67 + 5 * i] = f"b_pempty{i}"
 for i in range(5):
     names[90 + i] = f"b_land{i}"
+for i in range(3):
+    names[110 + i] = f"c_ld0_{i}"
+    names[113 + i] = f"c_loop_{i}"
+    names[116 + i] = f"c7_done{i}"
 for cta in (0, 1, 77, 147):
     row = t[cta]
     ev = sorted((int(v - base), names.get(k, str(k))) for k, v in enumerate(row) if v >= base and v != 0)
