@@ -76,28 +76,34 @@ densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restri
     uint32_t cols[kQ];
 #pragma unroll
     for (int u = 0; u < kQ; ++u) {
-      const int64_t q = qb + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
+      const int q = static_cast<int>(qb) + static_cast<int>(threadIdx.x) + u * static_cast<int>(blockDim.x);
       cols[u] = q < qe ? __ldg(p.col_indices + pb + index_pos(q, shuffled)) : kSentinel;
     }
     cp_async_wait<0>();
     __syncthreads();
+    // positions and element offsets of a row fit 32 bits (n_true <= K < 2^31); strides are
+    // powers of two in every reference plan (tile k), so q / S and q % S are a shift and a mask
+    const bool s_pow2 = (S & (S - 1)) == 0;
+    const int s_sh = __ffs(S) - 1;
+    const int qb32 = static_cast<int>(qb);
 #pragma unroll
     for (int u = 0; u < kQ; ++u) {
-      const int64_t q = qb + threadIdx.x + static_cast<int64_t>(u) * blockDim.x;
+      const int q = qb32 + static_cast<int>(threadIdx.x) + u * static_cast<int>(blockDim.x);
       if (q >= qe) continue;
       const uint32_t col = cols[u];
       if (col >= static_cast<uint32_t>(p.K)) {
         if (col != kSentinel) flag_status(p.status, MC_STATUS_BAD_INDEX);
         continue;
       }
-      const int64_t c = static_cast<int64_t>(col) - k0;
+      const int c = static_cast<int>(static_cast<int64_t>(col) - k0);
       if (c < 0 || c >= kc) continue;
       // element (v, q) of the row: stride q / S, offset v * S + q % S (sparse_format.py:131-139)
-      const int64_t e0 = (q / S) * V * S + (q % S);
+      const int sq = s_pow2 ? (q >> s_sh) : q / S;
+      const int e0 = sq * V * S + (q - sq * S);
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         // element offset inside the staged run (fits 32 bits: <= kVB words)
-        const int eo = static_cast<int>(e0 - (qb * V)) + v * S;
+        const int eo = e0 - qb32 * V + v * S;
         int32_t x;
         if constexpr (LB == 8) {
           x = reinterpret_cast<const int8_t*>(vals)[eo + stage_skew];
