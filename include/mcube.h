@@ -109,9 +109,12 @@ int mc_spmm(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n,
 /* SpMM with a caller-provided device workspace (same contract as mc_spmm otherwise).
  * At moderate sparsity (stored*V >= 8% of M*K, M/N/K multiples of 128) the library
  * densifies the LHS into int8 chunk planes inside the workspace and runs an exact
- * tcgen05 GEMM; results are bit-identical to the gather path. mc_spmm_workspace
- * returns the bytes that path needs (0: the problem always runs on the gather
- * kernels and the workspace may be NULL). Replaces kernels.spmm (kernels.py:293-298). */
+ * tcgen05 GEMM; on the row-segment gather path with a 4-bit RHS the workspace holds a
+ * copy of the RHS with the low-nibble sign bits flipped (one operation less per gathered
+ * word). Results are bit-identical either way. mc_spmm_workspace returns the bytes the
+ * chosen path can use (0: the problem runs on the gather kernels without one and the
+ * workspace may be NULL; a smaller workspace than asked is simply not used).
+ * Replaces kernels.spmm (kernels.py:293-298). */
 int mc_spmm_workspace(const mc_srbcrs* lhs, const mc_dense* rhs, size_t* bytes);
 /* Which kernel mc_spmm_ws (with the workspace mc_spmm_workspace asked for) runs for this
  * problem -- for reports and profiling; the result never depends on it. */
