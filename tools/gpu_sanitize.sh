@@ -6,7 +6,7 @@ CS=/usr/local/cuda/bin/compute-sanitizer
 SEL='test_spmm_segment_path_vs_oracle or test_spmm_golden or test_sddmm_golden or test_device_packer or test_attention_parity_golden or test_sddmm_paths_vs_oracle or test_spmm_l8r8_paths_vs_oracle or test_spmm_dense_path_vs_oracle'
 for tool in memcheck racecheck synccheck; do
   timeout 1500 $CS --tool $tool --error-exitcode 9 --print-limit 50 \
-     python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "$SEL" -p no:cacheprovider \
+     python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py -m gpu -q -x -k "$SEL" -p no:cacheprovider \
      > gpurun_out/sanitizer_${tool}.log 2>&1
   echo "rc=$?" >> gpurun_out/sanitizer_${tool}.log
   timeout 900 $CS --tool $tool --error-exitcode 9 --print-limit 50 \
