@@ -186,17 +186,26 @@ class Ctx:
         from paper_2209_06979_b200 import _native as Nn
         self.torch, self.Nn = torch, Nn
         self.rank, self.world, self.local = dist_info()
-        if self.world > 1:
-            ndev = torch.cuda.device_count()
+        # MCUBE_BENCH_SHARED_DEVICE_TEST=1: a correctness exercise of the N > 1 code path on
+        # one GPU (ranks share the device, gloo collectives on host tensors); its line says so
+        # in "test_shared_device" and is never a multi-GPU measurement
+        self.shared_test = os.environ.get("MCUBE_BENCH_SHARED_DEVICE_TEST") == "1"
+        ndev = torch.cuda.device_count()
+        if self.world > 1 and not self.shared_test:
             if self.world > ndev or self.local >= ndev:
                 raise SystemExit(f"bench.py: refusing {self.world} ranks on {ndev} visible GPU(s) -- "
                                  "every rank needs its own device")
-        torch.cuda.set_device(self.local)
-        self.dev = torch.device("cuda", self.local)
+        idx = self.local % ndev if self.shared_test else self.local
+        torch.cuda.set_device(idx)
+        self.dev = torch.device("cuda", idx)
+        self.cdev = torch.device("cpu") if self.shared_test else self.dev  # collective tensors
         self.dist = None
         if self.world > 1:
             import torch.distributed as dist
-            dist.init_process_group("nccl", device_id=self.dev)
+            if self.shared_test:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
             self.dist = dist
         self.lib = Nn.lib()
         self.stream = torch.cuda.current_stream()
@@ -209,14 +218,14 @@ class Ctx:
     def max_over_ranks(self, x: float) -> float:
         if self.dist is None:
             return x
-        t = self.torch.tensor([x], device=self.dev, dtype=self.torch.float64)
+        t = self.torch.tensor([x], device=self.cdev, dtype=self.torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
     def all_true(self, ok: bool) -> bool:
         if self.dist is None:
             return ok
-        t = self.torch.tensor([1 if ok else 0], device=self.dev, dtype=self.torch.int32)
+        t = self.torch.tensor([1 if ok else 0], device=self.cdev, dtype=self.torch.int32)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
         return bool(t.item())
 
@@ -397,7 +406,7 @@ def bench_c2(ctx, args, status):
     ctx.barrier()
     timed(warm)
     ctx.barrier()
-    with ClockSampler(ctx.local) as clk:
+    with ClockSampler(ctx.dev.index) as clk:
         total_ms_local = timed(main)
     ctx.barrier()
     per_reps = 3
@@ -789,7 +798,7 @@ def run_ours(args):
     if c2["fault"] is not None:
         validation.update(fault_injected=True, fault_detected=not c2["exact"])
     if ctx.world > 1:  # validation-only collective: every rank's output checksums
-        sums = torch.tensor(c2["checksums"], dtype=torch.int64, device=ctx.dev)
+        sums = torch.tensor(c2["checksums"], dtype=torch.int64, device=ctx.cdev)
         gathered = [torch.empty_like(sums) for _ in range(ctx.world)]
         ctx.dist.all_gather(gathered, sums)
         validation["checksums"] = [g.tolist() for g in gathered]
@@ -826,6 +835,8 @@ def run_ours(args):
                   "int8_kind": int8["kind"]},
     }
     line.update(extra)
+    if ctx.shared_test:
+        line["test_shared_device"] = True
     if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
         f = reference_figures(3, 1, budget_s=10.0)
         line["cpu_baseline"] = {k: f[k] for k in ("value", "unit", "cores", "kind", "sample", "one_core_tops",
