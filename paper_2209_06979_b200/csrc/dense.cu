@@ -16,7 +16,9 @@ namespace mcube {
 namespace {
 
 constexpr int kKC = 4096;  // densified columns per block (shared-memory row chunk)
-constexpr int kVB = 4096;  // staged value words per batch (16 KB)
+// staged value words per batch: ~2048 positions' worth (a C3 row at 70 % sparsity has 1229),
+// at most 16 KB -- small stages let V = 2 / 4 blocks reach 8 per SM (one wave fewer)
+__host__ __device__ constexpr int densify_vb(int v, int lb) { return v * lb * 64 < 4096 ? v * lb * 64 : 4096; }
 
 // value position q of a row -> stored index position (SHUFFLE_PERMUTATION^-1, sparse_format.py:222-230)
 __device__ __forceinline__ int64_t index_pos(int64_t q, bool shuffled) {
@@ -31,6 +33,7 @@ template <int LB, int V>
 __global__ void __launch_bounds__(256)
 densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restrict__ plane1) {
   constexpr int LC = LB >= 12 ? 2 : 1;
+  constexpr int kVB = densify_vb(V, LB);
   extern __shared__ __align__(16) uint8_t sm[];  // [LC][V][kKC] planes + kVB staged value words
   if (threadIdx.x == 0) pdl_launch_dependents();
   pdl_wait();
@@ -172,7 +175,7 @@ __global__ void widen_kernel(const uint32_t* __restrict__ words, int64_t n16, in
 template <int LB, int V>
 cudaError_t launch_densify_v(const SpmmParams& p, int8_t* a0, int8_t* a1, cudaStream_t s) {
   constexpr int LC = LB >= 12 ? 2 : 1;
-  const int smem = LC * V * kKC + kVB * 4;
+  const int smem = LC * V * kKC + densify_vb(V, LB) * 4;
   auto k = densify_kernel<LB, V>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(static_cast<unsigned>(p.vrows), static_cast<unsigned>((p.K + kKC - 1) / kKC));
@@ -197,7 +200,7 @@ cudaError_t launch_densify_l(const SpmmParams& p, int8_t* a0, int8_t* a1, cudaSt
 // the gather kernels.
 bool densify_stride_ok(const SpmmParams& p) {
   if (p.S <= 0 || p.V <= 0 || p.LB <= 0) return false;
-  int64_t per_batch = (static_cast<int64_t>(kVB) * 32 - 32) / (static_cast<int64_t>(p.V) * p.LB);
+  int64_t per_batch = (static_cast<int64_t>(densify_vb(p.V, p.LB)) * 32 - 32) / (static_cast<int64_t>(p.V) * p.LB);
   if (per_batch > 8 * 256) per_batch = 8 * 256;  // kQ positions per thread x 256 threads
   return per_batch / p.S * p.S >= p.S;
 }
