@@ -626,13 +626,14 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
     // (mma.sync m16n8k32: M = 16 head dims per MMA, 4 per k-step; N = 8 query rows)
     const uint8_t* vbl = reinterpret_cast<const uint8_t*>(vw + b * head_words) + (lane & 3) * 16;
     const uint32_t vring_s = smem_u32(vring);
-    uint32_t goff[2];  // slot * 64 + swizzled chunk of this lane's copies (u even / odd)
-    {
-      const int k0 = lane >> 2, ch = lane & 3;
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        goff[e] = 64 * (4 * (k0 & 3) + (k0 >> 2) + 2 * e) + ((ch * 16) ^ (32 * e));
-    }
+    // gathered V row kk of a k-step sits in slot kk (64 bytes), its 16-byte chunk c (head
+    // dims 16c..16c+15) at c ^ ((kk >> 1) & 3): the copies (8 lanes = 2 rows x 4 chunks) and
+    // the ldmatrix phases (8 rows, one chunk) both hit 8 distinct bank groups. This lane
+    // copies chunk lane & 3 of rows lane / 4 + 8u, i.e. at goff + 512 u.
+    const uint32_t goff = 64 * (lane >> 2) + (((lane & 3) ^ ((lane >> 3) & 3)) << 4);
+    // this lane's ldmatrix row (k = lane) of a slot; chunk c at c ^ ((lane >> 1) & 3)
+    const uint32_t loff = 64 * lane;
+    const int lsw = (lane >> 1) & 3;
     int acc[4][4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -643,15 +644,14 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
       if (!cached) { __syncwarp(); compute(j0, jn); }
       const int jpad = (jn + 31) & ~31;
       // gather of k-step s into ring slot s & 1: copy u of this lane moves 16-byte chunk
-      // ch = lane & 3 of gathered row kk = lane / 4 + 8u (slot order + XOR swizzle as
-      // spmm.cu; the per-lane slot offsets are hoisted in goff). The column padding of ix
-      // (column 0) pairs with P = 0, so the copies are unconditional.
+      // ch = lane & 3 of gathered row kk = lane / 4 + 8u. The column padding of ix (column 0)
+      // pairs with P = 0, so the copies are unconditional.
       auto gather = [&](int s) {
         const uint32_t base = vring_s + (s & 1) * 2048;
         const uint32_t* ixs = ix + 32 * s + (lane >> 2);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-          cp_async16_full(base + goff[u & 1] + 1024 * (u >> 1), vbl + static_cast<size_t>(ixs[8 * u]) * 64);
+          cp_async16_full(base + goff + 512 * u, vbl + static_cast<size_t>(ixs[8 * u]) * 64);
         cp_async_commit();
       };
       const int nsteps = jpad >> 5;
@@ -676,45 +676,35 @@ score_softmax_kernel(const uint32_t* __restrict__ qw, const uint32_t* __restrict
         if (s_ + 1 < nsteps) cp_async_wait<1>();
         else cp_async_wait<0>();
         __syncwarp();
-        const uint8_t* sb = vring + (s_ & 1) * 2048;
+        const uint32_t sbs = vring_s + (s_ & 1) * 2048 + loff;
         // B operand: P[g][32 s + 16 h + 4 t .. +3]
         uint32_t bf[2];
 #pragma unroll
         for (int h = 0; h < 2; ++h) bf[h] = *reinterpret_cast<const uint32_t*>(pm + g * 32 + 16 * h + 4 * t);
-        // A operand: gathered rows, transposed to k-major words per head dim
-        uint32_t T[2][8];
+        // A operand: one ldmatrix.m16n16.x2.trans per 16 head dims -- the k-major fragment of
+        // V^T (m = g <-> dim 16c + g, m = g + 8 <-> dim 16c + g + 8), no register transposes
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t raw[4][2];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int slot = 16 * h + 4 * i + t;
-            const uint2 w = *reinterpret_cast<const uint2*>(sb + slot * 64 + ((g * 8) ^ (32 * (t >> 1))));
-            raw[i][0] = w.x;
-            raw[i][1] = w.y;
-          }
-          transpose4x4(raw[0][0], raw[1][0], raw[2][0], raw[3][0], T[h][0], T[h][1], T[h][2], T[h][3]);
-          transpose4x4(raw[0][1], raw[1][1], raw[2][1], raw[3][1], T[h][4], T[h][5], T[h][6], T[h][7]);
+        for (int c = 0; c < 4; ++c) {
+          uint32_t a[4];
+          ldsm_t16x2(sbs + ((c ^ lsw) << 4), a[0], a[1], a[2], a[3]);
+          mma16832<false, false>(acc[c], a[0], a[1], a[2], a[3], bf[0], bf[1]);
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)  // m = g <-> dim 8g + 2q, m = g + 8 <-> dim 8g + 2q + 1
-          mma16832<false, false>(acc[q], T[0][2 * q], T[0][2 * q + 1], T[1][2 * q], T[1][2 * q + 1], bf[0], bf[1]);
         __syncwarp();
       }
     }
-    // epilogue: fp16(mix * alpha_m) (attention.py:169-176); acc[q]: (dim 8g+2q, v 2t), (8g+2q, 2t+1),
-    // (8g+2q+1, 2t), (8g+2q+1, 2t+1)
+    // epilogue: fp16(mix * alpha_m) (attention.py:169-176); acc[c]: (dim 16c+g, v 2t),
+    // (16c+g, 2t+1), (16c+g+8, 2t), (16c+g+8, 2t+1)
     const double am = alpha_m[b];
     const float am_f = static_cast<float>(am);
 #pragma unroll
     for (int vv = 0; vv < 2; ++vv) {
       const int v = 2 * t + vv;
-      uint32_t h4[4];
+      uint16_t* o = out_f16 + (b * L + r * 8 + v) * 64 + g;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        h4[q] = static_cast<uint32_t>(f16_dequant(acc[q][vv], am, am_f)) |
-                (static_cast<uint32_t>(f16_dequant(acc[q][2 + vv], am, am_f)) << 16);
-      *reinterpret_cast<uint4*>(out_f16 + (b * L + r * 8 + v) * 64 + 8 * g) = make_uint4(h4[0], h4[1], h4[2], h4[3]);
+      for (int c = 0; c < 4; ++c) {
+        o[16 * c] = f16_dequant(acc[c][vv], am, am_f);
+        o[16 * c + 8] = f16_dequant(acc[c][2 + vv], am, am_f);
+      }
     }
     return;
   }

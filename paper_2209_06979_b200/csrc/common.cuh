@@ -94,6 +94,18 @@ __device__ __forceinline__ void mma16832(int (&d)[4], uint32_t a0, uint32_t a1, 
   }
 }
 
+// ldmatrix.m16n16.x2.trans.b8 (LDSM.8.MT1616.2): lanes 0-15 give the 16-byte rows k = 0..15
+// of matrix 0, lanes 16-31 rows k = 16..31 of matrix 1; lane (g, t) receives bytes (row k,
+// column g) / (k, g + 8) for k = 4t..4t+3 of matrix 0 in r0 / r1 and of matrix 1 in r2 / r3:
+// exactly the m16n8k32 A fragment of the 16 x 32 transpose (tools/micro/ldsm_probe.cu,
+// profiles/r02s3_ldsm_layout.json).
+// Used by the row-segment SpMM consumer and the attention P x V step.
+__device__ __forceinline__ void ldsm_t16x2(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m16n16.x2.trans.shared.b8 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

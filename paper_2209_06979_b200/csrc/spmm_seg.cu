@@ -64,17 +64,6 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
       "l"(src), "r"(static_cast<int>(zero)));
 }
 
-// ldmatrix.m16n16.x2.trans.b8 (LDSM.8.MT1616.2): lanes 0-15 give the 16-byte rows k = 0..15
-// of matrix 0, lanes 16-31 rows k = 16..31 of matrix 1; lane (g, t) receives bytes (row k,
-// column g) / (k, g + 8) for k = 4t..4t+3 of matrix 0 in r0 / r1 and of matrix 1 in r2 / r3:
-// exactly the m16n8k32 A fragment of the 16 x 32 transpose (tools/micro/ldsm_probe.cu,
-// profiles/r02s3_ldsm_layout.json)
-__device__ __forceinline__ void ldsm_t16x2(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m16n16.x2.trans.shared.b8 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-
 // B ^ 0x08 in every byte (the low nibble's sign bit): 4-bit right-hand sides enter the
 // segment kernel's y' MMA without a per-use XOR
 __global__ void seg_prexor_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16) {
