@@ -290,12 +290,15 @@ __device__ __forceinline__ uint4 quant16_f16(uint4 u0, uint4 u1, double scale, f
 }
 
 // One 8-CTA cluster per [L x d] fp16 tensor (grid (8 * batch, 3) = Q, K, V of each head):
-// each CTA holds its 1/8 slice in registers, the slice maxima meet through distributed
-// shared memory (|x| max, attention.py:52-54; exact in fp32 for fp16 magnitudes), and the
-// slice is quantised from registers -- one HBM read and one int8 write per element. The
-// last of a head's three rank-0 CTAs (per-head arrival counter, reset for the next launch)
-// derives alpha_s (:147) and alpha_m (:169).
-constexpr int kQuantThreads = 512, kQuantCluster = 8, kQuantVec = 8;  // 8 x 16 B per thread
+// each CTA stages its 1/8 slice (up to kQuantSmem bytes; a larger remainder is streamed from
+// global twice) in shared memory with one bulk copy (the copy engine keeps 64 KB per CTA,
+// three CTAs per SM, in flight -- the register-tile version held two), the slice maxima meet
+// through distributed shared memory (|x| max, attention.py:52-54; exact in fp32 for fp16
+// magnitudes), and the slice is quantised from shared memory -- one HBM read and one int8
+// write per element. The last of a head's three rank-0 CTAs (per-head arrival counter, reset
+// for the next launch) derives alpha_s (:147) and alpha_m (:169).
+constexpr int kQuantThreads = 256, kQuantCluster = 8;
+constexpr int kQuantSmem = 64 * 1024;  // staged slice bytes per CTA
 __device__ __forceinline__ void st_cluster_f32(const float* local_addr, uint32_t rank, float v) {
   uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local_addr)), ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
@@ -305,12 +308,14 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 template <bool FAST>
-__global__ void __cluster_dims__(kQuantCluster, 1, 1) __launch_bounds__(kQuantThreads, 2)
+__global__ void __cluster_dims__(kQuantCluster, 1, 1) __launch_bounds__(kQuantThreads, 3)
 absquant_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n, int smax, int head_dim,
                     double* scales, double* alpha_s, double* alpha_m, uint32_t* out, int64_t words_per,
                     int64_t batch, uint32_t* arrivals) {
+  extern __shared__ __align__(128) uint8_t qsm[];  // the staged slice: groups of 2 x uint4
   __shared__ float red[kQuantThreads / 32];
   __shared__ float slice_max[kQuantCluster];
+  __shared__ __align__(8) uint64_t qbar;
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int64_t b = blockIdx.x / kQuantCluster;
@@ -320,18 +325,23 @@ absquant_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n
   // slice: 16-element groups [g0, g1) of this CTA; group g = 2 uint4 of input, 1 of output
   const int64_t n16 = n / 16;
   const int64_t g0 = n16 * rank / kQuantCluster, g1 = n16 * (rank + 1) / kQuantCluster;
-  uint4 u[kQuantVec];
-  float m = 0.f;
-  __half2 m2 = __float2half2_rn(0.f);
-#pragma unroll
-  for (int i = 0; i < kQuantVec / 2; ++i) {
-    const int64_t g = g0 + threadIdx.x + static_cast<int64_t>(i) * kQuantThreads;
-    const bool ok = g < g1;
-    u[2 * i] = ok ? __ldg(src + 2 * g) : make_uint4(0u, 0u, 0u, 0u);
-    u[2 * i + 1] = ok ? __ldg(src + 2 * g + 1) : make_uint4(0u, 0u, 0u, 0u);
+  const int64_t held = (g1 - g0) < kQuantSmem / 32 ? (g1 - g0) : kQuantSmem / 32;
+  const uint32_t bar = smem_u32(&qbar), sq = smem_u32(qsm);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // slices larger than the register tile (n > 8 * 16 * 512 * 4) are streamed twice
-  for (int64_t g = g0 + threadIdx.x + static_cast<int64_t>(kQuantVec / 2) * kQuantThreads; g < g1; g += kQuantThreads) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = static_cast<uint32_t>(held * 32);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    if (bytes)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(sq), "l"(src + 2 * g0), "r"(bytes), "r"(bar) : "memory");
+  }
+  float m = 0.f;
+  // slices larger than the stage: the remainder's maximum while the bulk copy lands
+  for (int64_t g = g0 + held + threadIdx.x; g < g1; g += kQuantThreads) {
     const uint4 w[2] = {__ldg(src + 2 * g), __ldg(src + 2 * g + 1)};
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -343,9 +353,17 @@ absquant_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n
       }
     }
   }
-#pragma unroll
-  for (int i = 0; i < kQuantVec; ++i) {
-    const __half2* h = reinterpret_cast<const __half2*>(&u[i]);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "QW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t"
+      "@!P1 bra QW_%=;\n}" ::"r"(bar)
+      : "memory");
+  const uint4* s4 = reinterpret_cast<const uint4*>(qsm);
+  __half2 m2 = __float2half2_rn(0.f);
+  for (int i = threadIdx.x; i < 2 * held; i += kQuantThreads) {
+    const uint4 u = s4[i];
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
     for (int x = 0; x < 4; ++x) m2 = __hmax2(m2, __habs2(h[x]));  // exact on fp16
   }
@@ -370,12 +388,9 @@ absquant_f16_kernel(const __half* q, const __half* k, const __half* v, int64_t n
   const double md = static_cast<double>(m);
   const double scale = md > 0.0 ? md / 127.0 : 1.0;
   const float inv_f = static_cast<float>(1.0 / scale);
-#pragma unroll
-  for (int i = 0; i < kQuantVec / 2; ++i) {
-    const int64_t g = g0 + threadIdx.x + static_cast<int64_t>(i) * kQuantThreads;
-    if (g < g1) dst[g] = quant16_f16<FAST>(u[2 * i], u[2 * i + 1], scale, inv_f);
-  }
-  for (int64_t g = g0 + threadIdx.x + static_cast<int64_t>(kQuantVec / 2) * kQuantThreads; g < g1; g += kQuantThreads)
+  for (int64_t i = threadIdx.x; i < held; i += kQuantThreads)
+    dst[g0 + i] = quant16_f16<FAST>(s4[2 * i], s4[2 * i + 1], scale, inv_f);
+  for (int64_t g = g0 + held + threadIdx.x; g < g1; g += kQuantThreads)
     dst[g] = quant16_f16<FAST>(__ldg(src + 2 * g), __ldg(src + 2 * g + 1), scale, inv_f);
   if (rank == 0 && threadIdx.x == 0) {
     scales[b * 4 + which] = scale;
@@ -793,7 +808,8 @@ cudaError_t launch_attention(const mc_attention_args* a, uint32_t* status, cudaS
     uint32_t* arrivals = reinterpret_cast<uint32_t*>(ws + o_amax);
     cudaMemsetAsync(arrivals, 0, B * 4, stream);
     auto kq = fast ? absquant_f16_kernel<true> : absquant_f16_kernel<false>;
-    kq<<<dim3(static_cast<unsigned>(B * kQuantCluster), 3), kQuantThreads, 0, stream>>>(
+    cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, kQuantSmem);
+    kq<<<dim3(static_cast<unsigned>(B * kQuantCluster), 3), kQuantThreads, kQuantSmem, stream>>>(
         static_cast<const __half*>(a->q), static_cast<const __half*>(a->k), static_cast<const __half*>(a->v), n, smax,
         a->head_dim, scales, alpha_s, alpha_m, qkv, qwords, B, arrivals);
     count_launch();
