@@ -64,7 +64,6 @@ struct SddmmTcParams {
   int64_t f16_stride;
   uint32_t* status;
   int n_panels, n_ctiles;
-  int tw;  // pattern columns per tile (<= 128 MMA rows)
   int64_t tiles;
   int debug;
 };

@@ -277,14 +277,14 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     if (warp == 0 && lane == 0) {
       for (int kb = 0; kb < KB; ++kb) {
         tc::tma_prefetch_2d(&tmA, kb * KBLK, static_cast<int>(c.item * p.M + c.panel * PANEL));
-        tc::tma_prefetch_2d(&tmB, kb * KBLK, static_cast<int>(c.item * p.N + c.ct * p.tw));
+        tc::tma_prefetch_2d(&tmB, kb * KBLK, static_cast<int>(c.item * p.N + c.ct * kCols));
       }
     } else if (warp >= kFirstBuild && warp < kFirstBuild + kBW && (lane & (kLanesPerRow - 1)) == 0) {
       const long long r = c.panel * VR + rl;
       if (r < p.vrows) {
         tc::prefetch_l2(p.row_offsets + r);
         const long long g = (r * p.n_blocks) / p.vrows +
-                            static_cast<long long>((static_cast<double>(c.ct * p.tw) / p.N) *
+                            static_cast<long long>((static_cast<double>(c.ct * kCols) / p.N) *
                                                    (static_cast<double>(p.n_blocks) / p.vrows));
         tc::prefetch_l2(p.col_indices + (g < p.n_blocks ? g : 0));
       }
@@ -303,7 +303,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     tc::mbar_arrive_expect_tx(full_bar(0), KB * kCols * KBLK);
     for (int kb = 0; kb < KB; ++kb)
       tc::tma_load_2d(sbase + L::OFF_B + kb * kCols * KBLK, &tmB, full_bar(0), kb * KBLK,
-                      static_cast<int>(c.item * p.N + c.ct * p.tw));
+                      static_cast<int>(c.item * p.N + c.ct * kCols));
   }
   MC_STAMP(threadIdx.x == 0, 102);
   long long lo = 0, b_lo = 0, b_hi = 0, spec_lo = -1, spec_hi = -1;
@@ -314,7 +314,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   if (warp >= kFirstBuild && warp < kFirstBuild + kBW && t0 < t1) {
     const int64_t rem0 = t0 % tiles_per_item;
     b_r = (rem0 / p.n_ctiles) * VR + rl;
-    b_c00 = static_cast<uint32_t>((rem0 % p.n_ctiles) * p.tw);
+    b_c00 = static_cast<uint32_t>((rem0 % p.n_ctiles) * kCols);
     if (b_r < p.vrows) {  // the first panel's row offsets: in flight across the setup barrier
       b_lo = p.row_offsets[b_r];
       b_hi = p.row_offsets[b_r + 1];
@@ -366,7 +366,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         tc::mbar_arrive_expect_tx(full_bar(s), KB * kCols * KBLK);
         for (int kb = 0; kb < KB; ++kb)
           tc::tma_load_2d(sbase + L::OFF_B + s * L::B_STAGE + kb * kCols * KBLK, &tmB, full_bar(s), kb * KBLK,
-                          static_cast<int>(item * p.N + ct * p.tw));
+                          static_cast<int>(item * p.N + ct * kCols));
         MC_STAMP(i < 6, 2 + static_cast<int>(i));
       }
     }
@@ -425,19 +425,12 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     // synchronisation: each warp arrives on the tile's pfull barrier.
     // (the speculative first window was issued before the setup barrier)
     int64_t cur_panel = -1;
-    const uint32_t tw = static_cast<uint32_t>(p.tw);
-    uint32_t qmask[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int nb = p.tw - 32 * x;
-      qmask[x] = nb >= 32 ? 0xffffffffu : (nb <= 0 ? 0u : (1u << nb) - 1u);
-    }
     TileCursor tc_(t0, p.n_panels, p.n_ctiles);
     for (int64_t t = t0; t < t1; ++t, tc_.next()) {
       const int i = static_cast<int>(t - t0);
       const int slot = i & (kRing - 1);
       const long long panel = tc_.panel, ct = tc_.ct, gpanel = tc_.gpanel;
-      const uint32_t c0 = static_cast<uint32_t>(ct * p.tw);
+      const uint32_t c0 = static_cast<uint32_t>(ct * kCols);
       if (gpanel != cur_panel) {
         // ---- segment start: locate the row's cursor at column c0 ----
         long long hi;
@@ -562,15 +555,7 @@ sddmm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 #pragma unroll
           for (int u = 0; u < 4; ++u) bad |= (c[u] - c0 < static_cast<uint32_t>(kCols)) && c[u] >= static_cast<uint32_t>(p.N);
         }
-        if (!__any_sync(0xffffffffu, c[3] - c0 < tw)) break;
-      }
-      // a tile narrower than the 128 MMA rows (p.tw < 128, finer last wave): columns
-      // [c0 + tw, c0 + 128) belong to the next tile
-      if (tw < 128u) {
-        w0 &= qmask[0];
-        w1 &= qmask[1];
-        w2 &= qmask[2];
-        w3 &= qmask[3];
+        if (!__any_sync(0xffffffffu, c[3] - c0 < static_cast<uint32_t>(kCols))) break;
       }
       MC_STAMP(lane == 0 && bw == 0 && i < 5, 65 + 5 * static_cast<int>(i));
       if (bad) flag_status(p.status, MC_STATUS_BAD_INDEX);
@@ -773,22 +758,12 @@ cudaError_t launch_sddmm_tc(const SddmmParams& p, cudaStream_t stream) {
   q.f16_stride = p.f16_stride;
   q.status = p.status;
   q.n_panels = static_cast<int>((p.M + vr * p.V - 1) / (vr * p.V));
+  q.n_ctiles = static_cast<int>((p.N + kCols - 1) / kCols);
+  q.tiles = static_cast<int64_t>(p.batch) * q.n_panels * q.n_ctiles;
   q.debug = getenv("MCUBE_DEBUG_TIMELINE") != nullptr;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // Tile width (pattern columns per tile, <= the 128 MMA rows). Narrower tiles even out the
-  // last wave (C2: 592 tiles of 112 = exactly 4 per SM instead of 512 of 128 = 3.46), but
-  // measured no faster (14.56 vs 14.57 us at 50 %: the per-launch prologue and the HBM write
-  // stream set the time, not the tile count), so 128 unless MCUBE_SDDMM_TW forces a width.
-  int tw = 128;
-  if (const char* e = getenv("MCUBE_SDDMM_TW")) {
-    const int w = atoi(e);
-    if (w >= 32 && w <= 128) tw = w;
-  }
-  q.tw = tw;
-  q.n_ctiles = static_cast<int>((p.N + tw - 1) / tw);
-  q.tiles = static_cast<int64_t>(p.batch) * q.n_panels * q.n_ctiles;
   const int grid = static_cast<int>(q.tiles < sms ? q.tiles : sms);
   if (grid == 0) return cudaSuccess;
   decltype(&sddmm_tc_kernel<8, 32>) kern;
