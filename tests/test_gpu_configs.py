@@ -181,3 +181,65 @@ def test_spmm_segment_path_vs_oracle(pair, n, v, sparsity, prexor, monkeypatch):
     want = O.spmm(sr.row_begin, sr.row_end, sr.col_indices, sr.values.to_values(), v, sr.stride, sr.shuffled, lb,
                   c["rhs"], rb, k)
     assert (out == want).all()
+
+
+def _segment_case_extreme(m, k, n, lb, stride, seed, vmax):
+    """Dense-ish rows with the extreme operand values the y' / h nibble decomposition has to
+    keep exact: LHS at +-(2^(lb-1)-1) or -2^(lb-1), RHS nibbles over the whole range
+    including -8 (sign bit of the low nibble set) and 7."""
+    rng = np.random.default_rng(seed)
+    v = 8
+    vr = m // v
+    lens = rng.integers(k // 2, k + 1, vr)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(k, size=int(x), replace=False)) for x in lens]).astype(np.uint32)
+    lo, hi = -(1 << (lb - 1)), (1 << (lb - 1)) - 1
+    vals = rng.choice(np.array([lo, hi, lo + 1, -1, 1, 0], dtype=np.int64), size=cols.size * v,
+                      p=[0.35, 0.35, 0.1, 0.08, 0.07, 0.05]) if vmax else rng.integers(lo, hi + 1, cols.size * v)
+    rhs = rng.choice(np.array([-8, 7, -7, -1, 0, 1], dtype=np.int64), size=(k, n), p=[0.3, 0.3, 0.1, 0.1, 0.1, 0.1])
+    b = mc.BcrsMatrix(m, k, v, offs, cols, mc.PackedArray.from_values(vals, lb))
+    sr = mc.shuffle_indices(mc.bcrs_to_srbcrs(b, stride))
+    return sr, rhs
+
+
+@pytest.mark.parametrize("prexor", ["1", "0"])
+@pytest.mark.parametrize("lb,stride", [(8, 32), (4, 32)])
+def test_spmm_segment_nibble_decomposition_extremes(lb, stride, prexor, monkeypatch):
+    """The row-segment kernel feeds a 4-bit RHS byte y to two MMAs (y ^ 0x08 and y & 0xF0)
+    and recovers the even column as acc(y') - acc(h) - 8 sum(a): exact at the extreme
+    operand values and with long rows (|sums| up to ~K * 128 * 8), with and without the
+    pre-XORed workspace copy."""
+    monkeypatch.setenv("MCUBE_SPMM_PATH", "seg")
+    monkeypatch.setenv("MCUBE_SEG_PREXOR", prexor)
+    m, k, n = 128, 8192, 512
+    sr, rhs = _segment_case_extreme(m, k, n, lb, stride, seed=lb + stride, vmax=True)
+    out = np.asarray(mc.spmm(mc.SpmmProblem(sr, mc.pack_dense(rhs, 4))))
+    want = O.spmm(sr.row_begin, sr.row_end, sr.col_indices, sr.values.to_values(), 8, stride, True, lb,
+                  rhs, 4, k)
+    assert (out == want).all()
+
+
+def test_spmm_segment_path_declines_beyond_its_int32_bound():
+    """|16 * sum| < 2^31 bounds the segment kernel's 4-bit forms: at K = 131104 (> 2^31 /
+    (16 * 1024)) an L8-R4 problem must not take it, and still matches the oracle."""
+    from paper_2209_06979_b200 import _device as Dv
+    from paper_2209_06979_b200 import _native as Nn
+    m, k, n = 64, 131104, 256
+    rng = np.random.default_rng(11)
+    vr = m // 8
+    lens = rng.integers(1, 64, vr)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    cols = np.concatenate([np.sort(rng.choice(k, size=int(x), replace=False)) for x in lens]).astype(np.uint32)
+    vals = rng.integers(-127, 128, cols.size * 8)
+    rhs = rng.integers(-8, 8, size=(k, n))
+    b = mc.BcrsMatrix(m, k, 8, offs, cols, mc.PackedArray.from_values(vals, 8))
+    sr = mc.shuffle_indices(mc.bcrs_to_srbcrs(b, 32))
+    p = mc.SpmmProblem(sr, mc.pack_dense(rhs, 4))
+    lhs_s, _k1 = Dv.srbcrs_struct(p.lhs)
+    rhs_s, _k2 = Dv.dense_struct(p.rhs)
+    pid = Nn.ctypes.c_int32(-1)
+    Nn.check(Nn.lib().mc_spmm_path(lhs_s, rhs_s, Nn.ctypes.byref(pid)))
+    assert pid.value != 1  # MC_SPMM_PATH_SEGMENT (include/mcube.h)
+    out = np.asarray(mc.spmm(p))
+    want = O.spmm(sr.row_begin, sr.row_end, sr.col_indices, sr.values.to_values(), 8, 32, True, 8, rhs, 4, k)
+    assert (out == want).all()
