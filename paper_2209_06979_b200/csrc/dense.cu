@@ -31,12 +31,16 @@ __device__ __forceinline__ int64_t index_pos(int64_t q, bool shuffled) {
 // [k0, k0 + kKC), built in shared memory, written as LC int8 planes [M x K].
 template <int LB, int V>
 __global__ void __launch_bounds__(256)
-densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restrict__ plane1) {
+densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restrict__ plane1, int after_widen) {
   constexpr int LC = LB >= 12 ? 2 : 1;
   constexpr int kVB = densify_vb(V, LB);
   extern __shared__ __align__(16) uint8_t sm[];  // [LC][V][kKC] planes + kVB staged value words
   if (threadIdx.x == 0) pdl_launch_dependents();
-  pdl_wait();
+  // after_widen: the previous kernel is widen_kernel, which released this grid only after
+  // every kernel before it completed (its own griddepcontrol.wait), so the SR-BCRS inputs
+  // are ready and the two passes overlap; the wait moves to the end so that this grid
+  // completes after widen does (the GEMM's griddepcontrol.wait then covers both)
+  if (!after_widen) pdl_wait();
   const int64_t r = blockIdx.x;
   const int64_t k0 = static_cast<int64_t>(blockIdx.y) * kKC;
   const int kc = static_cast<int>((p.K - k0 < kKC) ? p.K - k0 : kKC);
@@ -141,6 +145,7 @@ densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restri
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
+  if (after_widen) pdl_wait();
 }
 
 // packed R-bit RHS [K x N] -> RC int8 planes (R4: sign-extended nibbles; R16: low byte
@@ -148,6 +153,8 @@ densify_kernel(const SpmmParams p, int8_t* __restrict__ plane0, int8_t* __restri
 template <int RB>
 __global__ void widen_kernel(const uint32_t* __restrict__ words, int64_t n16, int8_t* __restrict__ plane0,
                              int8_t* __restrict__ plane1) {
+  pdl_wait();  // every earlier kernel complete before densify_kernel (dependent) is released
+  if (threadIdx.x == 0) pdl_launch_dependents();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n16) return;
   if constexpr (RB == 4) {
@@ -173,23 +180,23 @@ __global__ void widen_kernel(const uint32_t* __restrict__ words, int64_t n16, in
 }
 
 template <int LB, int V>
-cudaError_t launch_densify_v(const SpmmParams& p, int8_t* a0, int8_t* a1, cudaStream_t s) {
+cudaError_t launch_densify_v(const SpmmParams& p, int8_t* a0, int8_t* a1, cudaStream_t s, int after_widen) {
   constexpr int LC = LB >= 12 ? 2 : 1;
   const int smem = LC * V * kKC + densify_vb(V, LB) * 4;
   auto k = densify_kernel<LB, V>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   dim3 grid(static_cast<unsigned>(p.vrows), static_cast<unsigned>((p.K + kKC - 1) / kKC));
-  const cudaError_t e = launch_pdl(k, grid, dim3(256), smem, s, p, a0, a1);
+  const cudaError_t e = launch_pdl(k, grid, dim3(256), smem, s, p, a0, a1, after_widen);
   count_launch();
   return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int LB>
-cudaError_t launch_densify_l(const SpmmParams& p, int8_t* a0, int8_t* a1, cudaStream_t s) {
+cudaError_t launch_densify_l(const SpmmParams& p, int8_t* a0, int8_t* a1, cudaStream_t s, int after_widen) {
   switch (p.V) {
-    case 2: return launch_densify_v<LB, 2>(p, a0, a1, s);
-    case 4: return launch_densify_v<LB, 4>(p, a0, a1, s);
-    default: return launch_densify_v<LB, 8>(p, a0, a1, s);
+    case 2: return launch_densify_v<LB, 2>(p, a0, a1, s, after_widen);
+    case 4: return launch_densify_v<LB, 4>(p, a0, a1, s, after_widen);
+    default: return launch_densify_v<LB, 8>(p, a0, a1, s, after_widen);
   }
 }
 
@@ -227,26 +234,28 @@ cudaError_t launch_dense_spmm(SpmmParams p, void* workspace, cudaStream_t stream
   const int8_t* b0 = reinterpret_cast<const int8_t*>(p.rhs_words);
   const int8_t* b1 = nullptr;
   cudaError_t e;
-  switch (p.LB) {
-    case 4: e = launch_densify_l<4>(p, a0, a1, stream); break;
-    case 8: e = launch_densify_l<8>(p, a0, a1, stream); break;
-    case 12: e = launch_densify_l<12>(p, a0, a1, stream); break;
-    default: e = launch_densify_l<16>(p, a0, a1, stream); break;
-  }
-  if (e != cudaSuccess) return e;
+  // widen (R4 / R16) first: densify then runs alongside it (densify_kernel's after_widen)
   if (p.RB != 8) {
     const size_t plane_b = static_cast<size_t>(p.K) * p.N;
     int8_t* w0 = reinterpret_cast<int8_t*>(bws);
     int8_t* w1 = p.RB == 16 ? w0 + plane_b : nullptr;
     const int64_t n16 = static_cast<int64_t>(plane_b / 16);
     const unsigned grid = static_cast<unsigned>((n16 + 255) / 256);
-    if (p.RB == 4) widen_kernel<4><<<grid, 256, 0, stream>>>(p.rhs_words, n16, w0, w1);
-    else widen_kernel<16><<<grid, 256, 0, stream>>>(p.rhs_words, n16, w0, w1);
+    if (p.RB == 4) e = launch_pdl(widen_kernel<4>, dim3(grid), dim3(256), 0, stream, p.rhs_words, n16, w0, w1);
+    else e = launch_pdl(widen_kernel<16>, dim3(grid), dim3(256), 0, stream, p.rhs_words, n16, w0, w1);
     count_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (e != cudaSuccess) return e;
     b0 = w0;
     b1 = w1;
   }
+  const int after_widen = p.RB != 8 ? 1 : 0;
+  switch (p.LB) {
+    case 4: e = launch_densify_l<4>(p, a0, a1, stream, after_widen); break;
+    case 8: e = launch_densify_l<8>(p, a0, a1, stream, after_widen); break;
+    case 12: e = launch_densify_l<12>(p, a0, a1, stream, after_widen); break;
+    default: e = launch_densify_l<16>(p, a0, a1, stream, after_widen); break;
+  }
+  if (e != cudaSuccess) return e;
   return launch_gemm_tc(p, a0, a1, b0, b1, stream);
 }
 
