@@ -242,6 +242,19 @@ class Ctx:
         torch.cuda.synchronize()
         return g
 
+    def upload(self, g) -> str:
+        """cudaGraphUpload of an instantiated graph before it is timed: the first launch of a
+        graph otherwise uploads its 1000 kernel nodes inside the timed region (measured
+        +7.6 us per C2 step, tools/c2_order_probe.py). No kernel of the graph runs here."""
+        try:
+            from cuda.bindings import runtime as cudart
+            err = cudart.cudaGraphUpload(cudart.cudaGraphExec_t(g.raw_cuda_graph_exec()),
+                                         cudart.cudaStream_t(self.stream.cuda_stream))
+            self.torch.cuda.synchronize()
+            return "cudaGraphUpload" if int(err[0]) == 0 else f"cudaGraphUpload failed ({err[0]})"
+        except Exception as ex:  # no cuda-python: the first replay carries the upload
+            return f"not uploaded ({type(ex).__name__})"
+
     def time_flushed(self, g, reps: int) -> float:
         """Median device time (ms) of graph g, L2 flushed before every replay (events bracket
         the replay only), 2 untimed replays first; max over ranks."""
@@ -405,6 +418,7 @@ def bench_c2(ctx, args, status):
 
     ctx.barrier()
     timed(warm)
+    graph_upload = ctx.upload(main)  # the graph's upload is setup, not a step: outside the timing
     ctx.barrier()
     with ClockSampler(ctx.dev.index) as clk:
         total_ms_local = timed(main)
@@ -420,7 +434,8 @@ def bench_c2(ctx, args, status):
     value = ops_step * ctx.world * args.steps / (total_ms * 1e-3) / 1e12
     checksums = [int(pr["copies"][0][3].to(torch.int64).sum().item()) for pr in probs]
     return dict(probs=probs, value=value, total_ms=total_ms, per_launch=per_launch, launches=launches,
-                clocks=clk.summary(), step_copies=step_copies, exact=exact, fault=fault, checksums=checksums)
+                clocks=clk.summary(), step_copies=step_copies, exact=exact, fault=fault, checksums=checksums,
+                graph_upload=graph_upload)
 
 
 def run_e2e(ctx, args, probs, fault=None):
@@ -821,7 +836,9 @@ def run_ours(args):
                    "global_batch": ctx.world, "launches_per_step": len(probs),
                    "l2": f"cold: inputs larger than L2 ({c2['step_copies']} rotating device copies of the "
                          f"sweep's operands and outputs, >= {COLD_BYTES >> 20} MiB per rotation)",
-                   "parallelism": f"row panels x{ctx.world}" if ctx.world > 1 else "1 GPU"},
+                   "parallelism": f"row panels x{ctx.world}" if ctx.world > 1 else "1 GPU",
+                   "timing": "one CUDA graph of all steps x 5 launches, uploaded (" + c2["graph_upload"] +
+                             ") before the timed replay"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": load_traffic("sddmm_c2_s0.50"),
                      "kernel": "sddmm_tc_kernel<8, 32> (tcgen05 kind::i8) @ sparsity 0.50",
