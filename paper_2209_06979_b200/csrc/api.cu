@@ -207,7 +207,8 @@ int mc_spmm_ws(const mc_srbcrs* lhs, const mc_dense* rhs, int32_t bs_n, int32_t*
   if (workspace && need > 0 && workspace_bytes >= need)
     return cuda_status(launch_dense_spmm(p, workspace, s), "mc_spmm_ws");
   const size_t seg = need > 0 ? 0 : spmm_seg_workspace(p);
-  if (workspace && seg > 0 && workspace_bytes >= seg)
+  // the pre-XORed copy is gathered with 16-byte cp.async: a misaligned workspace is not used
+  if (workspace && seg > 0 && workspace_bytes >= seg && (reinterpret_cast<uintptr_t>(workspace) & 15) == 0)
     return cuda_status(launch_spmm_seg_ws(p, workspace, s), "mc_spmm_ws");
   return cuda_status(launch_spmm(p, s), "mc_spmm_ws");
 }
